@@ -1,0 +1,153 @@
+// C-ABI entry points of libzipccl_b200.so (declared in include/zipccl_b200.h).
+// Plain pointers and sizes only; all device work is enqueued on the caller's
+// stream and nothing here synchronises.
+#include <cstring>
+#include "zc_common.cuh"
+
+namespace zc {
+cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
+                                     double*, cudaStream_t);
+cudaError_t launch_codebook_modal(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
+                                  cudaStream_t);
+cudaError_t launch_encode(const uint16_t*, const EncodeSegs&, const uint8_t*, uint8_t*, void*,
+                          uint64_t*, cudaStream_t);
+cudaError_t launch_decode(const DecodeSegs&, uint16_t*, int32_t*, void*, int, cudaStream_t);
+}  // namespace zc
+
+using namespace zc;
+
+namespace {
+constexpr int kStatusBadArg = -1;
+constexpr int kStatusWorkspace = -2;
+constexpr int kStatusTooLarge = -3;
+
+int64_t tiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
+
+int status_of(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
+}  // namespace
+
+extern "C" {
+
+int zc_abi_version(void) { return 1; }
+
+int zc_tile_elements(void) { return kTile; }
+
+int zc_max_segments(void) { return kMaxSegments; }
+
+const char* zc_status_string(int status) {
+  switch (status) {
+    case 0: return "ok";
+    case kStatusBadArg: return "invalid argument";
+    case kStatusWorkspace: return "workspace too small";
+    case kStatusTooLarge: return "frame exceeds the u32 section-offset range";
+    default: return status > 0 ? cudaGetErrorString((cudaError_t)status) : "unknown status";
+  }
+}
+
+int64_t zc_static_bytes(int64_t n, int gs_log2) {
+  if (n < 1 || gs_log2 < 0 || gs_log2 > 30) return -1;
+  return layout_of(n, gs_log2).off[5];
+}
+
+int64_t zc_max_frame_bytes(int64_t n, int gs_log2) {
+  if (n < 1 || gs_log2 < 0 || gs_log2 > 30) return -1;
+  return layout_of(n, gs_log2).off[5] + pad128(n);
+}
+
+int64_t zc_workspace_bytes(int64_t total_elems, int nseg) {
+  if (total_elems < 0 || nseg < 0) return -1;
+  const int64_t tiles = total_elems / kTile + nseg + 1;
+  return 128 + 32 * tiles + 4096;
+}
+
+int zc_codebook_measured(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n, int nseg,
+                         void* ws, int64_t ws_bytes, uint8_t* book_dev, double* result_dev,
+                         cudaStream_t stream) {
+  if (nseg < 0 || nseg > kMaxSegments || !book_dev || !result_dev || !ws) return kStatusBadArg;
+  StatSegs s{};
+  int k = 0;
+  int64_t total = 0;
+  s.tile_start[0] = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (seg_n[i] < 0) return kStatusBadArg;
+    if (seg_n[i] == 0) continue;
+    s.x_off[k] = seg_off[i];
+    s.n[k] = seg_n[i];
+    s.tile_start[k + 1] = s.tile_start[k] + tiles_of(seg_n[i]);
+    total += seg_n[i];
+    ++k;
+  }
+  s.nseg = k;
+  if (k > 0 && !x) return kStatusBadArg;
+  if (128 + 32 * s.tile_start[k] > ws_bytes) return kStatusWorkspace;
+  return status_of(launch_codebook_measured(x, s, total, ws, book_dev, result_dev, stream));
+}
+
+int zc_codebook_modal(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n, int nseg,
+                      void* ws, int64_t ws_bytes, uint8_t* book_dev, cudaStream_t stream) {
+  if (nseg < 0 || nseg > kMaxSegments || !book_dev || !ws) return kStatusBadArg;
+  StatSegs s{};
+  int k = 0;
+  int64_t total = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (seg_n[i] < 0) return kStatusBadArg;
+    if (seg_n[i] == 0) continue;
+    s.x_off[k] = seg_off[i];
+    s.n[k] = seg_n[i];
+    s.tile_start[k + 1] = s.tile_start[k] + tiles_of(seg_n[i]);
+    total += seg_n[i];
+    ++k;
+  }
+  s.nseg = k;
+  if (k > 0 && !x) return kStatusBadArg;
+  if (128 + 2048 > ws_bytes) return kStatusWorkspace;
+  return status_of(launch_codebook_modal(x, s, total, ws, book_dev, stream));
+}
+
+int zc_encode(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
+              const int64_t* frame_off, int nseg, const uint8_t* book_dev, int gs_log2,
+              uint8_t* frames, void* ws, int64_t ws_bytes, uint64_t* frame_len_dev,
+              cudaStream_t stream) {
+  if (nseg < 1 || nseg > kMaxSegments || !x || !book_dev || !frames || !ws || !frame_len_dev)
+    return kStatusBadArg;
+  if (gs_log2 < 0 || gs_log2 > 30) return kStatusBadArg;
+  EncodeSegs s{};
+  s.nseg = nseg;
+  s.gs_log2 = gs_log2;
+  s.tile_start[0] = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (seg_n[i] < 1 || seg_off[i] < 0 || frame_off[i] < 0) return kStatusBadArg;
+    if ((reinterpret_cast<uintptr_t>(frames + frame_off[i]) & (kAlign - 1)) != 0) return kStatusBadArg;
+    if (layout_of(seg_n[i], gs_log2).off[5] > int64_t(0xFFFFFFFF)) return kStatusTooLarge;
+    s.x_off[i] = seg_off[i];
+    s.n[i] = seg_n[i];
+    s.frame_off[i] = frame_off[i];
+    s.tile_start[i + 1] = s.tile_start[i] + tiles_of(seg_n[i]);
+  }
+  if (128 + 8 * s.tile_start[nseg] > ws_bytes) return kStatusWorkspace;
+  return status_of(launch_encode(x, s, book_dev, frames, ws, frame_len_dev, stream));
+}
+
+int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64_t* dyn_len,
+              const int64_t* n, const int64_t* out_off, int nseg, uint16_t* out, int32_t* err_dev,
+              void* ws, int64_t ws_bytes, int write_out, cudaStream_t stream) {
+  if (nseg < 1 || nseg > kMaxSegments || !stat || !dyn || !n || !err_dev || !ws) return kStatusBadArg;
+  if (write_out && (!out || !out_off)) return kStatusBadArg;
+  DecodeSegs s{};
+  s.nseg = nseg;
+  s.tile_start[0] = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (n[i] < 1 || !stat[i]) return kStatusBadArg;
+    if ((reinterpret_cast<uintptr_t>(stat[i]) & 15) != 0) return kStatusBadArg;
+    s.stat[i] = stat[i];
+    s.dyn[i] = dyn[i];   // null: dynamic section follows the static part in place
+    s.dyn_len[i] = dyn_len ? dyn_len[i] : -1;
+    s.n[i] = n[i];
+    s.out_off[i] = out_off ? out_off[i] : 0;
+    s.tile_start[i + 1] = s.tile_start[i] + tiles_of(n[i]);
+  }
+  if (128 + 8 * s.tile_start[nseg] > ws_bytes) return kStatusWorkspace;
+  return status_of(launch_decode(s, out, err_dev, ws, write_out, stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,188 @@
+// Shared definitions for the ZipCCL B200 kernels (sm_100a).
+//
+// Frame layout (reference container.py:3-22, :45-95; codec.py:357-401):
+//   [0,128)            header "<4sBBBBQQ7sB6I" (56 B) + zero pad
+//   [off0, +n)         sign-mantissa bytes           ((w>>8)&0x80)|(w&0x7F)
+//   [off1..off3)       three LSB-first code planes   ceil(n/8) B each
+//   [off4, +4*groups)  u32 exclusive escape prefix per group (group_index)
+//   [off5, +zc)        escaped raw exponent bytes, element order
+// every section 128-aligned and zero padded; static part = [0, off5).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define ZC_HD __host__ __device__ __forceinline__
+
+namespace zc {
+
+constexpr int kAlign = 128;
+constexpr int kHeaderBytes = 56;
+constexpr int kMaxSegments = 64;
+
+// Tile geometry shared by encode / decode / stats.
+constexpr int kThreads = 256;               // 8 warps
+constexpr int kEPT = 16;                    // elements per thread (two 16-B loads)
+constexpr int kTile = kThreads * kEPT;      // 4096 elements per tile
+constexpr int kWarps = kThreads / 32;
+
+ZC_HD int64_t pad128(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+  int64_t n;
+  int gs_log2;
+  int64_t off[6];   // sm, p0, p1, p2, gi, zero_exponents
+  int64_t plane_bytes, groups;
+};
+
+// reference container.section_offsets (container.py:52-62)
+ZC_HD Layout layout_of(int64_t n, int gs_log2) {
+  Layout L;
+  L.n = n;
+  L.gs_log2 = gs_log2;
+  L.plane_bytes = (n + 7) >> 3;
+  L.groups = (n + (int64_t(1) << gs_log2) - 1) >> gs_log2;
+  int64_t pos = pad128(kHeaderBytes);
+  const int64_t sizes[5] = {n, L.plane_bytes, L.plane_bytes, L.plane_bytes, 4 * L.groups};
+  for (int i = 0; i < 5; ++i) { L.off[i] = pos; pos += pad128(sizes[i]); }
+  L.off[5] = pos;
+  return L;
+}
+
+// Error codes, ordered like the reference's check order (container.parse_header
+// :113-135, parse :138-180, CompressedChunk.check_structure/_check_consistency
+// codec.py:210-250) so that atomicMin reports the field the reference names.
+enum Err : int32_t {
+  kOk = 0,
+  kErrHeaderShort = 1,
+  kErrMagic = 2,
+  kErrVersion = 3,
+  kErrFlags = 4,
+  kErrGsLog2 = 5,
+  kErrElementCount = 6,
+  kErrZeroCountHeader = 7,
+  kErrCodebookDistinct = 8,
+  kErrCodebookBase = 9,
+  kErrOffset0 = 10,   // .. kErrOffset0 + 5
+  kErrFrameLength = 16,
+  kErrGroupIndex = 17,
+  kErrZeroCount = 18,
+  kErrCountMismatch = 19,   // collectives: header element_count != expected
+  kErrTimeout = 20,         // p2p: peer never signalled
+};
+
+// ---- memory-ordering helpers (decoupled look-back, peer flags) -------------
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
+               ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// Tile-status word for the decoupled look-back: flag in the top two bits,
+// inclusive/aggregate escape count in the low 62.
+constexpr uint64_t kFlagAgg = uint64_t(1) << 62;
+constexpr uint64_t kFlagInc = uint64_t(2) << 62;
+constexpr uint64_t kValMask = (uint64_t(1) << 62) - 1;
+
+// Warp 0 of a tile computes the exclusive prefix of `agg` over the tiles
+// [chain_first, tile) of its chain, publishing aggregate then inclusive.
+// `seed` is the prefix at the chain start (0 for encode, group_index for
+// decode chains).  Returns the exclusive prefix (lane 0 valid, all lanes
+// get it by shuffle).  Caller guarantees lower tile ids were acquired
+// earlier (atomic tile counter), so waiting cannot deadlock.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t tile,
+                                                  int64_t chain_first, uint64_t agg,
+                                                  uint64_t seed) {
+  const int lane = threadIdx.x & 31;
+  if (tile == chain_first) {
+    if (lane == 0) st_release_u64(status + tile, kFlagInc | ((seed + agg) & kValMask));
+    return seed;
+  }
+  if (lane == 0) st_release_u64(status + tile, kFlagAgg | (agg & kValMask));
+  uint64_t excl = 0;
+  int64_t p = tile - 1;
+  while (true) {
+    int64_t q = p - lane;
+    uint64_t s = 0;
+    bool in_chain = q >= chain_first;
+    if (in_chain) {
+      do { s = ld_acquire_u64(status + q); } while ((s >> 62) == 0);
+    }
+    // lanes past the chain start contribute nothing; treat the chain start
+    // as carrying an inclusive value (it always publishes one).
+    unsigned inc_mask = __ballot_sync(0xffffffffu, in_chain && (s & kFlagInc));
+    unsigned out_mask = __ballot_sync(0xffffffffu, !in_chain);
+    unsigned stop = inc_mask | out_mask;
+    int first_stop = stop ? __ffs(stop) - 1 : 32;   // closest lane that ends the walk
+    uint64_t v = (in_chain && lane <= first_stop) ? (s & kValMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (stop) break;
+    p -= 32;
+  }
+  if (lane == 0) st_release_u64(status + tile, kFlagInc | ((excl + agg) & kValMask));
+  return excl;
+}
+
+// Segment tables passed by value (A2A per-peer batching).
+struct EncodeSegs {
+  int nseg;
+  int gs_log2;
+  int64_t tile_start[kMaxSegments + 1];   // prefix of per-segment tile counts
+  int64_t x_off[kMaxSegments];            // element offset into x
+  int64_t n[kMaxSegments];                // elements (>= 1)
+  int64_t frame_off[kMaxSegments];        // byte offset of frame in frames
+};
+
+struct StatSegs {
+  int nseg;
+  int64_t tile_start[kMaxSegments + 1];
+  int64_t x_off[kMaxSegments];
+  int64_t n[kMaxSegments];
+};
+
+struct DecodeSegs {
+  int nseg;
+  int64_t tile_start[kMaxSegments + 1];
+  const uint8_t* stat[kMaxSegments];      // frame start (header)
+  const uint8_t* dyn[kMaxSegments];       // zero-exponent section start (null: in place)
+  int64_t dyn_len[kMaxSegments];          // bytes available in dyn (-1 unknown)
+  int64_t n[kMaxSegments];                // expected element count
+  int64_t out_off[kMaxSegments];          // element offset into out
+};
+
+__device__ __forceinline__ int find_seg(const int64_t* tile_start, int nseg, int64_t tile) {
+  int s = 0;
+  while (s + 1 < nseg && tile >= tile_start[s + 1]) ++s;
+  return s;
+}
+
+}  // namespace zc

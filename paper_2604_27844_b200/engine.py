@@ -1,0 +1,165 @@
+"""Device-level operations over the C-ABI: stats -> codebook, encode, decode.
+
+These are stream-ordered and never synchronise with the host; the public
+codec/container/collectives modules build the reference API on top.
+All tensors are CUDA tensors; BF16 words travel as int16 (same bits).
+"""
+
+from __future__ import annotations
+
+import functools
+
+import torch
+
+from . import _lib
+from ._lib import check, i64s, lib, ptrs, stream_ptr
+
+WORD = torch.int16
+
+
+def words_view(t: torch.Tensor) -> torch.Tensor:
+    """Flat contiguous int16 view of a BF16-word tensor (bits, not values)."""
+    if t.dtype in (torch.bfloat16, torch.float16, torch.uint16):
+        t = t.view(torch.int16)
+    elif t.dtype != torch.int16:
+        raise TypeError(f"expected a 16-bit BF16-word tensor, got {t.dtype}")
+    return t.contiguous().view(-1)
+
+
+def workspace(total_elems: int, nseg: int, device) -> torch.Tensor:
+    nbytes = int(lib().zc_workspace_bytes(int(total_elems), int(nseg)))
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+@functools.lru_cache(maxsize=1024)
+def _book_cached(entries: tuple, device_index: int) -> torch.Tensor:
+    return torch.tensor(list(entries) + [0], dtype=torch.uint8,
+                        device=torch.device("cuda", device_index))
+
+
+def book_tensor(entries, device) -> torch.Tensor:
+    """Device copy (uint8[8]) of a host-known codebook; cached."""
+    device = torch.device(device)
+    return _book_cached(tuple(int(e) for e in entries), device.index or 0)
+
+
+def measured_codebook(words: torch.Tensor, segs=None, stream=None):
+    """K1: sigma over the finite elements of the segments + on-device codebook.
+
+    Returns (book uint8[8], result float64[3] = sigma, finite count, path).
+    """
+    if segs is None:
+        segs = [(0, words.numel())]
+    dev = words.device
+    book = torch.empty(8, dtype=torch.uint8, device=dev)
+    result = torch.empty(3, dtype=torch.float64, device=dev)
+    total = sum(n for _, n in segs)
+    ws = workspace(total, len(segs), dev)
+    st = check(lib().zc_codebook_measured(
+        words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
+        i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
+        result.data_ptr(), stream_ptr(stream)), "zc_codebook_measured")
+    del st
+    return book, result
+
+
+def modal_codebook(words: torch.Tensor, segs=None, stream=None) -> torch.Tensor:
+    """Histogram-mode codebook (reference codec.py:181-185) for explicit bad sigma."""
+    if segs is None:
+        segs = [(0, words.numel())]
+    dev = words.device
+    book = torch.empty(8, dtype=torch.uint8, device=dev)
+    total = sum(n for _, n in segs)
+    ws = workspace(total, len(segs), dev)
+    check(lib().zc_codebook_modal(
+        words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
+        i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
+        stream_ptr(stream)), "zc_codebook_modal")
+    return book
+
+
+def max_frame_bytes(n: int, gs_log2: int = 9) -> int:
+    return int(lib().zc_max_frame_bytes(int(n), int(gs_log2)))
+
+
+def static_bytes(n: int, gs_log2: int = 9) -> int:
+    return int(lib().zc_static_bytes(int(n), int(gs_log2)))
+
+
+def encode(words: torch.Tensor, segs, book: torch.Tensor, gs_log2: int,
+           frames: torch.Tensor, frame_offs, frame_len: torch.Tensor | None = None,
+           stream=None) -> torch.Tensor:
+    """K2/K4: one frame per segment, written at frames[frame_offs[i]:].
+
+    Returns int64[nseg] device tensor of frame lengths (bytes).
+    """
+    segs = list(segs)
+    nseg = len(segs)
+    if frame_len is None:
+        frame_len = torch.empty(nseg, dtype=torch.int64, device=words.device)
+    total = sum(n for _, n in segs)
+    ws = workspace(total, nseg, words.device)
+    for lo in range(0, nseg, _lib.MAX_SEGMENTS):
+        part = segs[lo:lo + _lib.MAX_SEGMENTS]
+        offs = list(frame_offs)[lo:lo + _lib.MAX_SEGMENTS]
+        check(lib().zc_encode(
+            words.data_ptr(), i64s(o for o, _ in part), i64s(n for _, n in part), i64s(offs),
+            len(part), book.data_ptr(), int(gs_log2), frames.data_ptr(), ws.data_ptr(),
+            ws.numel(), frame_len.data_ptr() + 8 * lo, stream_ptr(stream)), "zc_encode")
+    return frame_len
+
+
+def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_offs,
+           write_out: bool = True, err: torch.Tensor | None = None, stream=None,
+           device=None) -> torch.Tensor:
+    """K3/K5: decode (and validate) one frame per segment.
+
+    stat_ptrs/dyn_ptrs are raw device addresses (local or peer-mapped);
+    dyn_ptrs entries may be 0 for "dynamic section in place".  Returns the
+    int32[nseg] device error words (0x7F7F7F7F = ok).
+    """
+    nseg = len(counts)
+    dev = out.device if out is not None else torch.device(device or "cuda")
+    if err is None:
+        err = torch.empty(nseg, dtype=torch.int32, device=dev)
+    total = sum(int(c) for c in counts)
+    ws = workspace(total, nseg, dev)
+    for lo in range(0, nseg, _lib.MAX_SEGMENTS):
+        hi = lo + _lib.MAX_SEGMENTS
+        check(lib().zc_decode(
+            ptrs(stat_ptrs[lo:hi]), ptrs(dyn_ptrs[lo:hi]),
+            i64s(dyn_lens[lo:hi]) if dyn_lens is not None else None,
+            i64s(counts[lo:hi]), i64s(out_offs[lo:hi]) if out_offs is not None else None,
+            len(counts[lo:hi]), out.data_ptr() if out is not None else None,
+            err.data_ptr() + 4 * lo, ws.data_ptr(), ws.numel(), 1 if write_out else 0,
+            stream_ptr(stream)), "zc_decode")
+    return err
+
+
+ERR_OK = 0x7F7F7F7F
+
+# error code -> (field, detail) in reference wording (container.py:113-180,
+# codec.py:210-250)
+_SECTION = ("sign_mantissa", "plane0", "plane1", "plane2", "group_index", "zero_exponents")
+ERR_FIELDS = {
+    1: ("header", "frame is shorter than the header"),
+    2: ("magic", "expected b'ZCCL'"),
+    3: ("version", "unsupported version"),
+    4: ("flags", "unknown flag bits"),
+    5: ("group_size_log2", "implausible value"),
+    6: ("element_count", "must be >= 1"),
+    7: ("zero_count", "exceeds element_count"),
+    8: ("codebook", "entries are not pairwise distinct"),
+    9: ("codebook", "base byte disagrees with first entry"),
+    **{10 + i: (f"{name} offset", "not the canonical offset") for i, name in enumerate(_SECTION)},
+    16: ("frame length", "does not match the header"),
+    17: ("group_index", "disagrees with escape counts in planes"),
+    18: ("zero_count", "planes disagree with zero_exponents"),
+    19: ("element_count", "frame holds a different element count than expected"),
+    20: ("timeout", "peer frame never became ready"),
+}
+
+
+def err_message(code: int) -> str:
+    field, detail = ERR_FIELDS.get(int(code), ("frame", f"error {code}"))
+    return f"{field}: {detail}"

@@ -1,0 +1,241 @@
+"""Parity of the CUDA codec with the reference (golden vectors made by the
+real reference) and with the CPU oracle.  Bit-exact: frames byte for byte,
+decoded words bit for bit."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import zc_oracle as zo
+from tests.conftest import GOLDEN, gaussian_words
+
+pytestmark = pytest.mark.gpu
+
+import paper_2604_27844_b200 as zc  # noqa: E402
+from paper_2604_27844_b200 import codec, container, engine  # noqa: E402
+from paper_2604_27844_b200.errors import CorruptChunkError, CorruptFrameError  # noqa: E402
+
+
+def host_words(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint16)
+
+
+def book_of(case, words):
+    src = case["book_src"]
+    if src == "given":
+        return codec.ExponentCodebook(tuple(case["book"]))
+    if src == "codebook_for":
+        return zc.codebook_for(words)
+    sigma = float(src.split("=")[1].rstrip(")"))
+    return zc.codebook_for(words, sigma)
+
+
+def test_golden_codec_cases(golden_meta, golden_arrays):
+    for i, case in enumerate(golden_meta["cases"]):
+        words = golden_arrays[f"w{i}"]
+        ref = golden_arrays[f"f{i}"].tobytes()
+        book = book_of(case, words)
+        assert list(book.entries) == case["book"], case["name"]
+        chunk = zc.compress(words, book, case["gs"])
+        assert chunk.zero_count == case["zc"], case["name"]
+        frame = zc.serialize(chunk)
+        assert frame == ref, case["name"]
+        assert np.array_equal(host_words(zc.decompress(chunk)), words), case["name"]
+        parsed = zc.parse(ref)
+        assert np.array_equal(host_words(zc.decompress(parsed)), words), case["name"]
+
+
+def test_sigma_cases(golden_meta):
+    for c in golden_meta["sigma_cases"]:
+        w = zo.gaussian(c["n"], c["s"], c["seed"])
+        got = zc.measure_sigma(w)
+        assert got == pytest.approx(c["sigma"], rel=1e-12, abs=0), c
+        assert list(zc.codebook_for(w).entries) == c["book"], c
+
+
+def test_sigma_special_values():
+    assert zc.measure_sigma(np.full(10, 0x3F80, np.uint16)) == 0.0
+    assert zc.measure_sigma(zo.from_f64(np.array([-1.0, 1.0]))) == 1.0
+    assert zc.measure_sigma(zo.from_f64(np.array([-1.0, 1.0, np.inf, np.nan]))) == 1.0
+    with pytest.raises(zc.DegenerateDataError):
+        zc.measure_sigma(np.empty(0, np.uint16))
+    with pytest.raises(zc.DegenerateDataError):
+        zc.measure_sigma(np.full(5, 0x7F80, np.uint16))
+
+
+@pytest.mark.parametrize("n", [4095, 4096, 4097, 1 << 20, (1 << 20) + 12345])
+def test_codebook_fallbacks_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    cases = [np.full(n, 0x3F80, np.uint16), np.zeros(n, np.uint16),
+             np.full(n, 0x7FC1, np.uint16)]
+    mixed = np.full(n, 0x4049, np.uint16)
+    mixed[rng.integers(0, n, n // 2 + 1)] = 0x7F80
+    cases.append(mixed)
+    cases.append(zo.gaussian(n, 3.0, seed=n))
+    for w in cases:
+        assert zc.codebook_for(w).entries == zo.book_for(w)
+        for s in (0.0, float("nan"), -2.0, float("inf")):
+            assert zc.codebook_for(w, s).entries == zo.book_for(w, s)
+
+
+def test_flip_outcomes_match_reference(golden_meta):
+    frame = np.load(GOLDEN / "flip_frame.npy")
+    arr = frame.copy()
+    for i, bit, outcome in golden_meta["flips"]:
+        arr[i] ^= bit
+        try:
+            zc.decompress(zc.parse(arr.tobytes()))
+            got = "ok"
+        except (CorruptFrameError, CorruptChunkError) as exc:
+            got = type(exc).__name__ + ":" + str(exc).split(":")[0]
+        arr[i] ^= bit
+        assert got == outcome, (i, bit)
+
+
+def test_c1_digest(golden_meta):
+    c1 = golden_meta["c1"]
+    w = zo.gaussian(1 << 24, 0.02, 0)
+    assert hashlib.sha256(w.tobytes()).hexdigest() == c1["input_sha256"]
+    assert zc.measure_sigma(w) == pytest.approx(c1["sigma"], rel=1e-12)
+    book = zc.codebook_for(w)
+    assert list(book.entries) == c1["book"]
+    chunk = zc.compress(w, book)
+    frame = zc.serialize(chunk)
+    assert len(frame) == c1["frame_len"]
+    assert hashlib.sha256(frame).hexdigest() == c1["frame_sha256"]
+    assert np.array_equal(host_words(zc.decompress(chunk)), w)
+
+
+def test_single_word_patterns_round_trip():
+    # every 16-bit pattern in its own 1-element frame, in- and out-of-book
+    # (reference tests/test_acceptance.py:123-140), batched 64 frames a launch
+    words = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    dev = torch.from_numpy(words.view(np.int16)).cuda()
+    for mode in ("in", "out"):
+        out = torch.empty_like(dev)
+        for lo in range(0, 65536, 64):
+            seg = list(range(lo, lo + 64))
+            exps = [(int(w) >> 7) & 0xFF for w in words[lo:lo + 64]]
+            assert len(set(exps)) == 1
+            e = exps[0]
+            if mode == "in":
+                first = min(e, 249)
+                book = tuple(range(first, first + 7))
+            else:
+                book = tuple((e + 8 + i) % 256 for i in range(7))
+            cap = engine.max_frame_bytes(1)
+            frames = torch.empty(64 * cap, dtype=torch.uint8, device="cuda")
+            flen = engine.encode(dev, [(i, 1) for i in seg], engine.book_tensor(book, "cuda"), 9,
+                                 frames, [k * cap for k in range(64)])
+            err = engine.decode([frames.data_ptr() + k * cap for k in range(64)], [0] * 64,
+                                None, [1] * 64, out, seg)
+            assert torch.all(err == engine.ERR_OK)
+            expect = 128 * 6 + (128 if mode == "out" else 0)
+            assert torch.all(flen == expect)
+        assert torch.equal(out, dev)
+
+
+def test_fuzz_buffers_against_oracle():
+    rng = np.random.default_rng(31)
+    derived = codec.derive_codebook(1.0)
+    for _ in range(100):
+        n = int(rng.integers(1, 20000))
+        w = rng.integers(0, 1 << 16, n).astype(np.uint16)
+        gs = int(1 << rng.integers(0, 15))
+        book = derived if rng.random() < 0.5 else codec.ExponentCodebook(
+            tuple(int(x) for x in rng.choice(256, 7, replace=False)))
+        frame = zc.serialize(zc.compress(w, book, gs))
+        assert frame == zo.encode(w, book.entries, gs)
+        assert np.array_equal(host_words(zc.decompress(zc.parse(frame))), w)
+
+
+@pytest.mark.parametrize("n", [1 << 27, 218112000 // 8, 5 * 4096 * 4096 + 3])
+def test_large_round_trip_properties(n):
+    # size-independent properties at benchmark scale: decode(encode(x)) == x,
+    # frame length law, escape count equals an independent torch count
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = (torch.randn(n, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    words = engine.words_view(x)
+    book = zc.codebook_for(x)
+    chunk = zc.compress(x, book)
+    e = (words.to(torch.int32) >> 7) & 0xFF
+    in_book = torch.zeros(256, dtype=torch.bool, device="cuda")
+    in_book[list(book.entries)] = True
+    esc = int((~in_book[e]).sum().item())
+    assert chunk.zero_count == esc
+    assert chunk.frame.numel() == codec.compressed_size_bytes(n, esc)
+    out = zc.decompress(chunk)
+    assert torch.equal(out, words)
+
+
+def test_group_random_access():
+    for n, gs in [(2000, 512), (2049, 512), (130, 64), (70000, 1 << 14)]:
+        data = gaussian_words(n, seed=n + 1)
+        chunk = zc.compress(data, codec.derive_codebook(1.0), group_size=gs)
+        for g in range((n + gs - 1) // gs):
+            got = host_words(zc.decompress_group(chunk, g))
+            assert np.array_equal(got, data[g * gs:(g + 1) * gs])
+    with pytest.raises(IndexError):
+        zc.decompress_group(zc.compress(gaussian_words(100), codec.derive_codebook(1.0)), 1)
+
+
+def test_chunk_from_sections_validation():
+    c = zc.compress(gaussian_words(2000, seed=42), codec.derive_codebook(1.0))
+    sm, planes, gi, ze = c.sign_mantissa, c.exp_planes, c.group_index, c.zero_exponents
+    bad = codec.CompressedChunk(c.element_count, c.group_size, c.codebook, sm, planes, gi,
+                                ze[:-1])
+    with pytest.raises(CorruptChunkError, match="zero_count"):
+        zc.decompress(bad)
+    bad = codec.CompressedChunk(c.element_count, c.group_size, c.codebook, sm,
+                                (planes[0][:-1], planes[1], planes[2]), gi, ze)
+    with pytest.raises(CorruptChunkError, match="exp_planes"):
+        zc.decompress(bad)
+    gi2 = gi.clone()
+    gi2[1] += 1
+    bad = codec.CompressedChunk(c.element_count, c.group_size, c.codebook, sm, planes, gi2, ze)
+    with pytest.raises(CorruptChunkError, match="group_index"):
+        zc.decompress(bad)
+    good = codec.CompressedChunk(c.element_count, c.group_size, c.codebook, sm, planes, gi, ze)
+    assert zc.serialize(good) == zc.serialize(c)
+
+
+def test_errors_and_dtypes():
+    with pytest.raises(ValueError):
+        zc.compress(np.empty(0, np.uint16), codec.derive_codebook(1.0))
+    with pytest.raises(ValueError):
+        zc.compress(gaussian_words(10), codec.derive_codebook(1.0), group_size=100)
+    x = torch.randn(3000, device="cuda").to(torch.bfloat16)
+    book = zc.codebook_for(x)
+    f1 = zc.serialize(zc.compress(x, book))
+    f2 = zc.serialize(zc.compress(x.view(torch.int16).cpu().numpy().view(np.uint16), book))
+    assert f1 == f2
+    out = zc.decompress(zc.parse(f1))
+    assert torch.equal(out.view(torch.bfloat16), x)
+
+
+def test_unaligned_segments_and_batched_frames(golden_meta, golden_a2a):
+    # the per-peer batched encoder (K4) on a2a send buffers, unaligned offsets
+    world = golden_meta["a2a"]["world"]
+    for rank in range(world):
+        chunks = [golden_a2a[f"r{rank}_c{q}"] for q in range(world)]
+        buf = np.concatenate(chunks)
+        offs = np.concatenate([[0], np.cumsum([c.size for c in chunks])])
+        dev = torch.from_numpy(buf.view(np.int16)).cuda()
+        segs = [(int(offs[q]), chunks[q].size) for q in range(world)
+                if q != rank and chunks[q].size]
+        peers = [q for q in range(world) if q != rank and chunks[q].size]
+        if not segs:
+            continue
+        book = codec.device_codebook(dev, None, segs)
+        caps = [engine.max_frame_bytes(n) for _, n in segs]
+        foffs = np.concatenate([[0], np.cumsum(caps)])[:-1]
+        frames = torch.empty(int(sum(caps)), dtype=torch.uint8, device="cuda")
+        flen = engine.encode(dev, segs, book, 9, frames, foffs).cpu().numpy()
+        host = frames.cpu().numpy()
+        for k, q in enumerate(peers):
+            got = host[foffs[k]:foffs[k] + flen[k]].tobytes()
+            assert got == golden_a2a[f"r{rank}_f{q}"].tobytes(), (rank, q)
