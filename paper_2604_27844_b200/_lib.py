@@ -15,7 +15,10 @@ import torch
 
 from .errors import ExtensionMissingError
 
-LIB_PATH = Path(__file__).resolve().parent / "libzipccl_b200.so"
+import os
+
+LIB_PATH = Path(os.environ.get("ZC_LIB_PATH") or
+                Path(__file__).resolve().parent / "libzipccl_b200.so")
 
 _lock = threading.Lock()
 _lib = None

@@ -12,6 +12,7 @@ cudaError_t launch_codebook_modal(const uint16_t*, const StatSegs&, int64_t, voi
 cudaError_t launch_encode(const uint16_t*, const EncodeSegs&, const uint8_t*, uint8_t*, void*,
                           uint64_t*, cudaStream_t);
 cudaError_t launch_decode(const DecodeSegs&, uint16_t*, int32_t*, void*, int, cudaStream_t);
+int64_t encode_workspace_bytes(int64_t ntiles);
 }  // namespace zc
 
 using namespace zc;
@@ -57,7 +58,9 @@ int64_t zc_max_frame_bytes(int64_t n, int gs_log2) {
 int64_t zc_workspace_bytes(int64_t total_elems, int nseg) {
   if (total_elems < 0 || nseg < 0) return -1;
   const int64_t tiles = total_elems / kTile + nseg + 1;
-  return 128 + 32 * tiles + 4096;
+  const int64_t a = 128 + 32 * tiles + 4096;
+  const int64_t b = encode_workspace_bytes(tiles);
+  return a > b ? a : b;
 }
 
 int zc_codebook_measured(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n, int nseg,
@@ -124,7 +127,7 @@ int zc_encode(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
     s.frame_off[i] = frame_off[i];
     s.tile_start[i + 1] = s.tile_start[i] + tiles_of(seg_n[i]);
   }
-  if (128 + 8 * s.tile_start[nseg] > ws_bytes) return kStatusWorkspace;
+  if (encode_workspace_bytes(s.tile_start[nseg]) > ws_bytes) return kStatusWorkspace;
   return status_of(launch_encode(x, s, book_dev, frames, ws, frame_len_dev, stream));
 }
 

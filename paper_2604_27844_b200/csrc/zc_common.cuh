@@ -71,6 +71,17 @@ enum Err : int32_t {
 };
 
 // ---- memory-ordering helpers (decoupled look-back, peer flags) -------------
+// The look-back status word carries its payload in the same 64-bit word as
+// its flag, so it needs coherence, not ordering: relaxed gpu-scope accesses
+// (no L1 invalidation / fence per poll, unlike ld.acquire / st.release).
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -105,6 +116,40 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return d;
 }
 
+// ---- TMA bulk copies + mbarriers (sm_90+ async proxy, used as the B200 ring) --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n ZC_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra ZC_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+// dst, src 16-B aligned; bytes a multiple of 16.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 // Tile-status word for the decoupled look-back: flag in the top two bits,
 // inclusive/aggregate escape count in the low 62.
 constexpr uint64_t kFlagAgg = uint64_t(1) << 62;
@@ -114,41 +159,58 @@ constexpr uint64_t kValMask = (uint64_t(1) << 62) - 1;
 // Warp 0 of a tile computes the exclusive prefix of `agg` over the tiles
 // [chain_first, tile) of its chain, publishing aggregate then inclusive.
 // `seed` is the prefix at the chain start (0 for encode, group_index for
-// decode chains).  Returns the exclusive prefix (lane 0 valid, all lanes
-// get it by shuffle).  Caller guarantees lower tile ids were acquired
+// decode chains).  Each lane inspects kLookbackPerLane predecessors, so one
+// L2 round trip covers a 256-tile window: the inclusive-prefix frontier then
+// advances 256 tiles per round trip instead of 32, which is what lets the
+// single-pass encoder keep up with HBM on B200 (a 32-wide window caps it at
+// ~0.45 G elements/ms).  Caller guarantees lower tile ids were claimed
 // earlier (atomic tile counter), so waiting cannot deadlock.
+constexpr int kLookbackPerLane = 8;
+
 __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t tile,
                                                   int64_t chain_first, uint64_t agg,
                                                   uint64_t seed) {
   const int lane = threadIdx.x & 31;
   if (tile == chain_first) {
-    if (lane == 0) st_release_u64(status + tile, kFlagInc | ((seed + agg) & kValMask));
+    if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | ((seed + agg) & kValMask));
     return seed;
   }
-  if (lane == 0) st_release_u64(status + tile, kFlagAgg | (agg & kValMask));
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagAgg | (agg & kValMask));
   uint64_t excl = 0;
-  int64_t p = tile - 1;
+  int64_t p = tile - 1;   // newest predecessor not yet accounted for
   while (true) {
-    int64_t q = p - lane;
-    uint64_t s = 0;
-    bool in_chain = q >= chain_first;
-    if (in_chain) {
-      do { s = ld_acquire_u64(status + q); } while ((s >> 62) == 0);
+    // lane l covers predecessors p - l*V - v, v = 0..V-1 (newest first)
+    uint64_t s[kLookbackPerLane];
+#pragma unroll
+    for (int v = 0; v < kLookbackPerLane; ++v) {
+      const int64_t q = p - (int64_t)lane * kLookbackPerLane - v;
+      s[v] = (q >= chain_first) ? ld_relaxed_u64(status + q) : kFlagInc;
     }
-    // lanes past the chain start contribute nothing; treat the chain start
-    // as carrying an inclusive value (it always publishes one).
-    unsigned inc_mask = __ballot_sync(0xffffffffu, in_chain && (s & kFlagInc));
-    unsigned out_mask = __ballot_sync(0xffffffffu, !in_chain);
-    unsigned stop = inc_mask | out_mask;
-    int first_stop = stop ? __ffs(stop) - 1 : 32;   // closest lane that ends the walk
-    uint64_t v = (in_chain && lane <= first_stop) ? (s & kValMask) : 0;
+#pragma unroll
+    for (int v = 0; v < kLookbackPerLane; ++v) {
+      const int64_t q = p - (int64_t)lane * kLookbackPerLane - v;
+      while ((s[v] >> 62) == 0) s[v] = ld_relaxed_u64(status + q);
+    }
+    // per lane: sum up to and including its newest inclusive entry
+    uint64_t part = 0;
+    bool hit = false;
+#pragma unroll
+    for (int v = 0; v < kLookbackPerLane; ++v) {
+      if (!hit) {
+        part += s[v] & kValMask;   // out-of-chain slots carry value 0
+        hit = (s[v] & kFlagInc) != 0;
+      }
+    }
+    const unsigned inc_mask = __ballot_sync(0xffffffffu, hit);
+    const int first = inc_mask ? __ffs(inc_mask) - 1 : 32;
+    uint64_t v = (lane <= first) ? part : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     excl += v;
-    if (stop) break;
-    p -= 32;
+    if (inc_mask) break;
+    p -= 32 * kLookbackPerLane;
   }
-  if (lane == 0) st_release_u64(status + tile, kFlagInc | ((excl + agg) & kValMask));
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | ((excl + agg) & kValMask));
   return excl;
 }
 

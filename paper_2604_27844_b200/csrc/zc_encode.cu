@@ -1,16 +1,21 @@
 // K2/K4 — single-pass frame encoder (reference codec.compress codec.py:264-305
 // fused with container.serialize container.py:65-95).
 //
-// One CTA = one 4096-element tile (256 threads x 16 elements).  A launch
-// covers one or more independent segments (the per-peer chunks of an
-// all-to-all); every segment gets its own frame and its own
-// decoupled look-back chain for the escape prefix.  Per element the work is
-// integer only:
-//   sign-mantissa byte  ((w>>8)&0x80)|(w&0x7F)       -> 1 B/elem, 16-B stores
-//   code = LUT[exponent] via a 256-entry "spread" table whose entry carries
-//   the three plane bits and the escape bit at bit positions 0/8/16/24, so
-//   8 elements OR into one register whose bytes are plane0/1/2/escape bytes
-//   group_index / escapes positioned by the look-back prefix.
+// Persistent kernel: grid = resident CTAs (SMs x occupancy); each CTA walks
+// 4096-element tiles (256 threads x 16 elements) acquired from an atomic
+// counter, so tile ids are handed out in order and the decoupled look-back
+// for the escape prefix cannot deadlock.  The next tile's 32 B/thread are
+// loaded while the current tile is processed, and the tile after that is
+// already claimed, so the look-back round trip overlaps memory traffic.
+//
+// A launch covers one or more independent segments (the per-peer chunks of
+// an all-to-all); every segment gets its own frame and its own
+// look-back chain.  Per element, integer only:
+//   sign-mantissa byte  ((w>>8)&0x80)|(w&0x7F)       -> 3 ops / 4 elements
+//   code = LUT[exponent] from a 256-entry "spread" table whose entry carries
+//   the three plane bits and the escape bit at bit positions 0/8/16/24, so 8
+//   elements accumulate into one register whose bytes are plane0/1/2/escape
+//   group_index / escapes placed by the look-back prefix.
 // Bytes per element: 2 read + ~1.40 written (HBM bound, no tensor cores).
 #include "zc_common.cuh"
 
@@ -30,203 +35,625 @@ __device__ __forceinline__ void write_header_and_pads(uint8_t* frame, const Layo
     else if (t >= 24 && t < 31) b = book[t - 24];
     else if (t == 31) b = book[0];
     else if (t >= 32 && t < 56) {
-      int i = (t - 32) >> 2;
-      b = (uint8_t)(uint32_t(L.off[i]) >> (8 * ((t - 32) & 3)));
+      const int i = (t - 32) >> 2;
+      int64_t o = 0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) o = (k == i) ? L.off[k] : o;
+      b = (uint8_t)(uint32_t(o) >> (8 * ((t - 32) & 3)));
     }
     frame[t] = b;
   }
   // zero pads behind every section
-  const int64_t ends[6] = {L.off[0] + L.n, L.off[1] + L.plane_bytes, L.off[2] + L.plane_bytes,
-                           L.off[3] + L.plane_bytes, L.off[4] + 4 * L.groups,
-                           L.off[5] + (int64_t)zc};
-  const int64_t lims[6] = {L.off[1], L.off[2], L.off[3], L.off[4], L.off[5],
-                           L.off[5] + pad128((int64_t)zc)};
+#pragma unroll
   for (int r = 0; r < 6; ++r) {
-    int64_t p = ends[r] + t;
-    if (p < lims[r]) frame[p] = 0;
+    const int64_t end = r == 0 ? L.off[0] + L.n
+                      : r < 4 ? L.off[r] + L.plane_bytes
+                      : r == 4 ? L.off[4] + 4 * L.groups
+                               : L.off[5] + (int64_t)zc;
+    const int64_t lim = r < 5 ? L.off[r + 1] : L.off[5] + pad128((int64_t)zc);
+    const int64_t p = end + t;
+    if (p < lim) frame[p] = 0;
+  }
+}
+
+struct TileWords {
+  uint32_t w[8];
+};
+
+__device__ __forceinline__ void load_words(const uint16_t* xs, int64_t base, int64_t nvalid,
+                                           TileWords& t) {
+  if (nvalid >= kEPT && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)) {
+    const uint4 a = ld_stream_v4(xs + base), b = ld_stream_v4(xs + base + 8);
+    t.w[0] = a.x; t.w[1] = a.y; t.w[2] = a.z; t.w[3] = a.w;
+    t.w[4] = b.x; t.w[5] = b.y; t.w[6] = b.z; t.w[7] = b.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t lo = (2 * k < nvalid) ? xs[base + 2 * k] : 0u;
+      const uint32_t hi = (2 * k + 1 < nvalid) ? xs[base + 2 * k + 1] : 0u;
+      t.w[k] = lo | (hi << 16);
+    }
   }
 }
 
 __global__ void __launch_bounds__(kThreads)
-encode_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs,
+encode_lookback_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs,
               const uint8_t* __restrict__ book, uint8_t* __restrict__ frames,
               uint64_t* __restrict__ status, unsigned* __restrict__ counter,
               uint64_t* __restrict__ frame_len) {
   __shared__ uint32_t s_lut[256];
   __shared__ __align__(16) uint8_t s_exp[kTile];     // per-thread exponent bytes
   __shared__ uint8_t s_esc[kTile];                   // compacted escapes of the tile
-  __shared__ uint32_t s_warp[kWarps];
-  __shared__ int64_t s_tile;
+  __shared__ __align__(16) uint32_t s_warp[kWarps];
+  __shared__ int64_t s_claim[1];
   __shared__ uint64_t s_excl;
   __shared__ uint8_t s_book[8];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = (int64_t)atomicAdd(counter, 1u);
+  const int64_t ntiles = segs.tile_start[segs.nseg];
   if (tid < 7) s_book[tid] = book[tid];
   __syncthreads();
   {
-    // spread LUT (codec.py:131-138 encode_table), bit0/8/16 = code bits, bit24 = escape
+    // spread LUT (codec.py:131-138 encode_table): bit0/8/16 = code bits, bit24 = escape
     uint32_t c = 0;
 #pragma unroll
     for (int i = 0; i < 7; ++i) c = (s_book[i] == tid) ? uint32_t(i + 1) : c;
     s_lut[tid] = (c & 1u) | ((c >> 1) & 1u) << 8 | ((c >> 2) & 1u) << 16 | uint32_t(c == 0) << 24;
   }
-  const int64_t tile = s_tile;
-  const int seg = find_seg(segs.tile_start, segs.nseg, tile);
+
+  int cseg = -1;
+  Layout L{};
+  uint8_t* frame = nullptr;
+  const uint16_t* xs = nullptr;
+  int64_t seg_t0 = 0, seg_tn = 0;
+  auto seg_of = [&](int64_t tile) {
+    const int s = find_seg(segs.tile_start, segs.nseg, tile);
+    if (s != cseg) {
+      cseg = s;
+      L = layout_of(segs.n[s], segs.gs_log2);
+      frame = frames + segs.frame_off[s];
+      xs = x + segs.x_off[s];
+      seg_t0 = segs.tile_start[s];
+      seg_tn = segs.tile_start[s + 1];
+    }
+  };
+
+  // Claim a tile, then process it straight away: the time from claim to the
+  // tile's aggregate being published is one load latency, independent of
+  // what other tiles this CTA holds, so look-back windows stay short.
+  while (true) {
+    if (tid == 0) s_claim[0] = (int64_t)atomicAdd(counter, 1u);
+    __syncthreads();                                      // (A) claim visible, smem reuse
+    const int64_t cur = s_claim[0];
+    if (cur >= ntiles) break;
+    TileWords cw;
+    seg_of(cur);
+    const int64_t t_local = cur - seg_t0;
+    const int64_t base = t_local * kTile + (int64_t)tid * kEPT;
+    const int64_t nvalid = L.n - base;
+    load_words(xs, base, nvalid, cw);
+    const bool full = nvalid >= kEPT;
+    const uint32_t* w = cw.w;
+
+    // ---- sign-mantissa bytes (codec.py:279) -------------------------------
+    uint32_t sm[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t p = prmt(w[2 * j], w[2 * j + 1], 0x6420);   // low bytes
+      const uint32_t q = prmt(w[2 * j], w[2 * j + 1], 0x7531);   // sign | e7..e1
+      sm[j] = (p & 0x7F7F7F7Fu) | (q & 0x80808080u);
+    }
+    // ---- exponent bytes (bf16.py:39-41), staged for the escape path -------
+    {
+      uint32_t e[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) e[j] = prmt(w[2 * j] >> 7, w[2 * j + 1] >> 7, 0x6420);
+      *reinterpret_cast<uint4*>(s_exp + tid * kEPT) = make_uint4(e[0], e[1], e[2], e[3]);
+    }
+    // ---- codes -> plane bytes + escape mask (codec.py:281-289) -------------
+    // LUT byte offset = exponent*4, formed as (w & mask) * 2^k >> 32 (IMAD.HI)
+    uint32_t A = 0, B = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t wl = w[k >> 1];
+      const uint32_t off = (k & 1) ? __umulhi(wl & 0x7F800000u, 1u << 11)
+                                   : __umulhi(wl & 0x00007F80u, 1u << 27);
+      A += *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(s_lut) + off) << k;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t wl = w[4 + (k >> 1)];
+      const uint32_t off = (k & 1) ? __umulhi(wl & 0x7F800000u, 1u << 11)
+                                   : __umulhi(wl & 0x00007F80u, 1u << 27);
+      B += *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(s_lut) + off) << k;
+    }
+    const uint32_t valid16 = full ? 0xFFFFu : (nvalid > 0 ? ((1u << nvalid) - 1u) : 0u);
+    if (!full) {
+      A &= (valid16 & 0xFFu) * 0x01010101u;
+      B &= ((valid16 >> 8) & 0xFFu) * 0x01010101u;
+    }
+    const uint32_t p0 = prmt(A, B, 0x40), p1 = prmt(A, B, 0x51), p2 = prmt(A, B, 0x62);
+    const uint32_t esc = prmt(A, B, 0x73) & 0xFFFFu;
+
+    // ---- static-section stores -------------------------------------------
+    if (full) {
+      st_stream_v4(frame + L.off[0] + base, make_uint4(sm[0], sm[1], sm[2], sm[3]));
+      const int64_t pb = base >> 3;
+      *reinterpret_cast<uint16_t*>(frame + L.off[1] + pb) = (uint16_t)p0;
+      *reinterpret_cast<uint16_t*>(frame + L.off[2] + pb) = (uint16_t)p1;
+      *reinterpret_cast<uint16_t*>(frame + L.off[3] + pb) = (uint16_t)p2;
+    } else if (nvalid > 0) {
+      for (int k = 0; k < nvalid; ++k)
+        frame[L.off[0] + base + k] = (uint8_t)(sm[k >> 2] >> (8 * (k & 3)));
+      const int64_t pb = base >> 3;
+      frame[L.off[1] + pb] = (uint8_t)p0;
+      frame[L.off[2] + pb] = (uint8_t)p1;
+      frame[L.off[3] + pb] = (uint8_t)p2;
+      if (nvalid > 8) {
+        frame[L.off[1] + pb + 1] = (uint8_t)(p0 >> 8);
+        frame[L.off[2] + pb + 1] = (uint8_t)(p1 >> 8);
+        frame[L.off[3] + pb + 1] = (uint8_t)(p2 >> 8);
+      }
+    }
+
+    // ---- tile-local exclusive scan of escape counts ------------------------
+    const uint32_t cnt = __popc(esc);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();                                      // (B) s_warp, s_exp ready
+    uint32_t wbase = 0, agg = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) {
+      const uint32_t v = s_warp[i];
+      wbase += (i < warp) ? v : 0u;
+      agg += v;
+    }
+    const uint32_t lp = wbase + incl - cnt;
+
+    // ---- compact escapes into shared memory (codec.py:283-284) -------------
+    {
+      uint32_t m = esc, pos = lp;
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        s_esc[pos++] = s_exp[tid * kEPT + k];
+      }
+    }
+    // ---- decoupled look-back: escapes before this tile in the segment ------
+    if (warp == 0) {
+#ifdef ZC_EXPERIMENT_NO_LOOKBACK
+      if (lane == 0) s_excl = 0;
+#else
+      const uint64_t ex = lookback_warp(status, cur, seg_t0, agg, 0);
+      if (lane == 0) s_excl = ex;
+#endif
+    }
+    __syncthreads();                                      // (C) s_excl, s_esc ready
+    const uint64_t excl = s_excl;
+
+    // ---- group index: exclusive escape prefix at every group start --------
+    if (nvalid > 0) {
+      uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
+      const int gsl = segs.gs_log2;
+      if (gsl >= 4) {
+        if ((base & ((int64_t(1) << gsl) - 1)) == 0) gi[base >> gsl] = (uint32_t)(excl + lp);
+      } else {
+        const int gs = 1 << gsl;
+        for (int j = 0; j < kEPT && j < nvalid; j += gs)
+          gi[(base + j) >> gsl] = (uint32_t)(excl + lp + __popc(esc & ((1u << j) - 1u)));
+      }
+    }
+    // ---- escapes out (dynamic section) -------------------------------------
+    {
+      uint8_t* dst = frame + L.off[5] + excl;
+      for (uint32_t i = tid; i < agg; i += kThreads) dst[i] = s_esc[i];
+    }
+    // ---- last tile of the segment: header, pads, frame length -------------
+    if (cur == seg_tn - 1) {
+      const uint64_t zc = excl + agg;
+      write_header_and_pads(frame, L, zc, s_book);
+      if (tid == 0) frame_len[cseg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
+    }
+  }
+}
+
+
+// ============================================================================
+// Two-kernel encoder for large inputs (the default above kLookbackMaxTiles).
+//
+// Pass 1 (encode_tiles_kernel) is the HBM-bound part and has no inter-CTA
+// dependence.  Persistent CTAs each own a contiguous run of tiles of one
+// segment; thread 0 keeps a kStages-deep ring of 8 KB input tiles in flight
+// with TMA bulk copies (cp.async.bulk + mbarrier complete_tx), so three tiles
+// per CTA are loading while one is encoded.  The CTA writes the sign-mantissa
+// and plane sections in place, group_index entries relative to its own run,
+// its escapes compacted into its scratch run, and its escape total.
+// Pass 2 (encode_fixup_kernel, one CTA per pass-1 CTA) sums the totals of
+// the runs before it (<= a few hundred values), adds that offset to its
+// group_index entries, moves its escapes to their final place with
+// coalesced copies, and the segment's last run writes header + pads.
+// Extra traffic: 2 x zero_count bytes (the scratch round trip).
+// ============================================================================
+
+constexpr int kStages = 4;
+constexpr int kStageBytes = kTile * 2;
+
+struct RunPlan {                      // pass-1 CTA -> (segment, tile run)
+  int nruns;
+  int run_start[kMaxSegments + 1];    // first run of each segment
+  int64_t tiles_per_run[kMaxSegments];
+};
+
+__device__ __forceinline__ void run_range(const EncodeSegs& segs, const RunPlan& rp, int run,
+                                          int& seg, int64_t& t_begin, int64_t& t_end) {
+  int sg = 0;
+  while (sg + 1 < segs.nseg && run >= rp.run_start[sg + 1]) ++sg;
+  seg = sg;
+  const int64_t r = run - rp.run_start[sg];
+  const int64_t seg_tiles = segs.tile_start[sg + 1] - segs.tile_start[sg];
+  t_begin = r * rp.tiles_per_run[sg];
+  t_end = t_begin + rp.tiles_per_run[sg];
+  if (t_begin > seg_tiles) t_begin = seg_tiles;
+  if (t_end > seg_tiles) t_end = seg_tiles;
+}
+
+// thread 0: TMA the full 16-B chunks of local tile `t` of segment `s`
+__device__ __forceinline__ void encode_issue(const uint16_t* xs, int64_t n, int64_t t,
+                                             uint8_t* stage, uint64_t* bar) {
+  const int64_t base = t * kTile;
+  const int64_t valid = n - base;
+  const uint32_t bytes = (uint32_t)((valid >= kTile ? kTile : valid) * 2) & ~15u;
+  if (((reinterpret_cast<uintptr_t>(xs) & 15) == 0) && bytes > 0) {
+    mbar_arrive_expect_tx(bar, bytes);
+    tma_load_1d(stage, xs + base, bytes, bar);
+  } else {
+    mbar_arrive(bar);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const RunPlan rp,
+                    const uint8_t* __restrict__ book, uint8_t* __restrict__ frames,
+                    uint8_t* __restrict__ scratch, uint64_t* __restrict__ run_total) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  uint8_t* ring = s_dyn;                                              // kStages x 8 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kStages * kStageBytes);
+  __shared__ uint32_t s_lut[256];
+  __shared__ __align__(16) uint32_t s_warp[kWarps];
+  __shared__ uint8_t s_book[8];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int seg;
+  int64_t t_begin, t_end;
+  run_range(segs, rp, blockIdx.x, seg, t_begin, t_end);
   const int64_t n = segs.n[seg];
   const Layout L = layout_of(n, segs.gs_log2);
   uint8_t* frame = frames + segs.frame_off[seg];
   const uint16_t* xs = x + segs.x_off[seg];
-  const int64_t t_local = tile - segs.tile_start[seg];
-  const int64_t base = t_local * kTile + (int64_t)tid * kEPT;
-  const int64_t nvalid = n - base;  // may be <= 0
-  const bool full = nvalid >= kEPT;
+  const bool aligned = (reinterpret_cast<uintptr_t>(xs) & 15) == 0;
+  uint8_t* esc_out = scratch + (segs.tile_start[seg] + t_begin) * kTile;
+  uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
+  const int gsl = segs.gs_log2;
+
+  if (tid < 7) s_book[tid] = book[tid];
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) mbar_init(bars + i, 1);
+    fence_mbar_init();
+    for (int i = 0; i < kStages; ++i)
+      if (t_begin + i < t_end) encode_issue(xs, n, t_begin + i, ring + i * kStageBytes, bars + i);
+  }
   __syncthreads();
-
-  // ---- load 16 words (two 16-B loads on the aligned fast path) ----------
-  uint32_t w[8];
-  if (full && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)) {
-    uint4 a = ld_stream_v4(xs + base), b = ld_stream_v4(xs + base + 8);
-    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-    w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-  } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      uint32_t lo = (2 * k < nvalid) ? xs[base + 2 * k] : 0u;
-      uint32_t hi = (2 * k + 1 < nvalid) ? xs[base + 2 * k + 1] : 0u;
-      w[k] = lo | (hi << 16);
-    }
-  }
-  const uint32_t valid16 = full ? 0xFFFFu : (nvalid > 0 ? ((1u << nvalid) - 1u) : 0u);
-
-  // ---- sign-mantissa bytes (codec.py:279) ---------------------------------
-  uint32_t sm[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint32_t p = prmt(w[2 * j], w[2 * j + 1], 0x6420);   // low byte of each word
-    uint32_t q = prmt(w[2 * j], w[2 * j + 1], 0x7531);   // high byte (sign | e7..e1)
-    sm[j] = (p & 0x7F7F7F7Fu) | (q & 0x80808080u);
-  }
-  // ---- exponent bytes (bf16.py:39-41) staged for the escape path ----------
   {
-    uint32_t e[4];
+    // spread LUT (codec.py:131-138 encode_table): bit0/8/16 = code bits, bit24 = escape
+    uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) e[j] = prmt(w[2 * j] >> 7, w[2 * j + 1] >> 7, 0x6420);
-    *reinterpret_cast<uint4*>(s_exp + tid * kEPT) = make_uint4(e[0], e[1], e[2], e[3]);
-  }
-  // ---- codes -> plane bytes + escape mask (codec.py:281-289) --------------
-  uint32_t A = 0, B = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t wl = w[k >> 1];
-    const uint32_t e = (k & 1) ? ((wl >> 23) & 0xFFu) : ((wl >> 7) & 0xFFu);
-    A |= s_lut[e] << k;
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t wl = w[4 + (k >> 1)];
-    const uint32_t e = (k & 1) ? ((wl >> 23) & 0xFFu) : ((wl >> 7) & 0xFFu);
-    B |= s_lut[e] << k;
-  }
-  if (!full) {
-    A &= (valid16 & 0xFFu) * 0x01010101u;
-    B &= ((valid16 >> 8) & 0xFFu) * 0x01010101u;
-  }
-  const uint32_t p0 = prmt(A, B, 0x40), p1 = prmt(A, B, 0x51), p2 = prmt(A, B, 0x62);
-  const uint32_t esc = prmt(A, B, 0x73) & 0xFFFFu;
-
-  // ---- static-section stores ----------------------------------------------
-  if (full) {
-    st_stream_v4(frame + L.off[0] + base, make_uint4(sm[0], sm[1], sm[2], sm[3]));
-    const int64_t pb = base >> 3;
-    *reinterpret_cast<uint16_t*>(frame + L.off[1] + pb) = (uint16_t)p0;
-    *reinterpret_cast<uint16_t*>(frame + L.off[2] + pb) = (uint16_t)p1;
-    *reinterpret_cast<uint16_t*>(frame + L.off[3] + pb) = (uint16_t)p2;
-  } else if (nvalid > 0) {
-    for (int k = 0; k < nvalid; ++k) frame[L.off[0] + base + k] = (uint8_t)(sm[k >> 2] >> (8 * (k & 3)));
-    const int64_t pb = base >> 3;
-    frame[L.off[1] + pb] = (uint8_t)p0;
-    frame[L.off[2] + pb] = (uint8_t)p1;
-    frame[L.off[3] + pb] = (uint8_t)p2;
-    if (nvalid > 8) {
-      frame[L.off[1] + pb + 1] = (uint8_t)(p0 >> 8);
-      frame[L.off[2] + pb + 1] = (uint8_t)(p1 >> 8);
-      frame[L.off[3] + pb + 1] = (uint8_t)(p2 >> 8);
-    }
-  }
-
-  // ---- tile-local exclusive scan of escape counts --------------------------
-  const uint32_t cnt = __popc(esc);
-  uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  uint32_t wbase = 0, agg = 0;
-#pragma unroll
-  for (int i = 0; i < kWarps; ++i) {
-    uint32_t v = s_warp[i];
-    wbase += (i < warp) ? v : 0u;
-    agg += v;
-  }
-  const uint32_t lp = wbase + incl - cnt;   // escapes in the tile before this thread
-
-  // ---- compact escapes into shared memory (codec.py:283-284) ---------------
-  {
-    uint32_t m = esc, pos = lp;
-    while (m) {
-      const int k = __ffs(m) - 1;
-      m &= m - 1;
-      s_esc[pos++] = s_exp[tid * kEPT + k];
-    }
-  }
-
-  // ---- decoupled look-back: escapes before this tile in the segment ---------
-  if (warp == 0) {
-    uint64_t ex = lookback_warp(status, tile, segs.tile_start[seg], agg, 0);
-    if (lane == 0) s_excl = ex;
+    for (int i = 0; i < 7; ++i) c = (s_book[i] == tid) ? uint32_t(i + 1) : c;
+    s_lut[tid] = (c & 1u) | ((c >> 1) & 1u) << 8 | ((c >> 2) & 1u) << 16 | uint32_t(c == 0) << 24;
   }
   __syncthreads();
-  const uint64_t excl = s_excl;
 
-  // ---- group index: exclusive escape prefix at every group start (:291-295)
-  if (nvalid > 0) {
-    uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
-    const int gsl = segs.gs_log2;
-    if (gsl >= 4) {
-      if ((base & ((int64_t(1) << gsl) - 1)) == 0) gi[base >> gsl] = (uint32_t)(excl + lp);
+  uint32_t run = 0;   // escapes of this run before the current tile
+  for (int64_t t = t_begin; t < t_end; ++t) {
+    const int64_t k = t - t_begin;
+    const int st = (int)(k % kStages);
+    const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
+    const int64_t base = t * kTile + (int64_t)tid * kEPT;
+    const int64_t nvalid = n - base;
+    const bool full = nvalid >= kEPT;
+    const int64_t tile_valid = n - t * kTile;
+    const int tma_elems = aligned ? (int)((((tile_valid >= kTile ? kTile : tile_valid) * 2) & ~15) / 2) : 0;
+
+    mbar_wait(bars + st, (uint32_t)((k / kStages) & 1));
+
+    uint32_t w[8];
+    const bool from_smem = full && tid * kEPT + kEPT <= tma_elems;
+    if (from_smem) {
+      const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
+      const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
     } else {
-      const int gs = 1 << gsl;
-      for (int j = 0; j < kEPT && j < nvalid; j += gs)
-        gi[(base + j) >> gsl] = (uint32_t)(excl + lp + __popc(esc & ((1u << j) - 1u)));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e0 = tid * kEPT + 2 * j;
+        uint32_t lo = 0, hi = 0;
+        if (2 * j < nvalid) lo = (e0 < tma_elems) ? tw[e0] : xs[base + 2 * j];
+        if (2 * j + 1 < nvalid) hi = (e0 + 1 < tma_elems) ? tw[e0 + 1] : xs[base + 2 * j + 1];
+        w[j] = lo | (hi << 16);
+      }
+    }
+
+    // ---- sign-mantissa bytes (codec.py:279) ---------------------------------
+    uint32_t sm[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t p = prmt(w[2 * j], w[2 * j + 1], 0x6420);
+      const uint32_t q = prmt(w[2 * j], w[2 * j + 1], 0x7531);
+      sm[j] = (p & 0x7F7F7F7Fu) | (q & 0x80808080u);
+    }
+    // ---- codes -> plane bytes + escape mask (codec.py:281-289) ---------------
+    uint32_t A = 0, B = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t wl = w[j >> 1];
+      const uint32_t off = (j & 1) ? __umulhi(wl & 0x7F800000u, 1u << 11)
+                                   : __umulhi(wl & 0x00007F80u, 1u << 27);
+      A += *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(s_lut) + off) << j;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t wl = w[4 + (j >> 1)];
+      const uint32_t off = (j & 1) ? __umulhi(wl & 0x7F800000u, 1u << 11)
+                                   : __umulhi(wl & 0x00007F80u, 1u << 27);
+      B += *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(s_lut) + off) << j;
+    }
+    if (!full) {
+      const uint32_t valid16 = nvalid > 0 ? ((1u << nvalid) - 1u) : 0u;
+      A &= (valid16 & 0xFFu) * 0x01010101u;
+      B &= ((valid16 >> 8) & 0xFFu) * 0x01010101u;
+    }
+    const uint32_t p0 = prmt(A, B, 0x40), p1 = prmt(A, B, 0x51), p2 = prmt(A, B, 0x62);
+    const uint32_t esc = prmt(A, B, 0x73) & 0xFFFFu;
+
+    if (full) {
+      st_stream_v4(frame + L.off[0] + base, make_uint4(sm[0], sm[1], sm[2], sm[3]));
+      const int64_t pb = base >> 3;
+      *reinterpret_cast<uint16_t*>(frame + L.off[1] + pb) = (uint16_t)p0;
+      *reinterpret_cast<uint16_t*>(frame + L.off[2] + pb) = (uint16_t)p1;
+      *reinterpret_cast<uint16_t*>(frame + L.off[3] + pb) = (uint16_t)p2;
+    } else if (nvalid > 0) {
+      for (int j = 0; j < nvalid; ++j)
+        frame[L.off[0] + base + j] = (uint8_t)(sm[j >> 2] >> (8 * (j & 3)));
+      const int64_t pb = base >> 3;
+      frame[L.off[1] + pb] = (uint8_t)p0;
+      frame[L.off[2] + pb] = (uint8_t)p1;
+      frame[L.off[3] + pb] = (uint8_t)p2;
+      if (nvalid > 8) {
+        frame[L.off[1] + pb + 1] = (uint8_t)(p0 >> 8);
+        frame[L.off[2] + pb + 1] = (uint8_t)(p1 >> 8);
+        frame[L.off[3] + pb + 1] = (uint8_t)(p2 >> 8);
+      }
+    }
+
+    // ---- tile-local scan ------------------------------------------------------
+    const uint32_t cnt = __popc(esc);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();                                      // (B)
+    uint32_t wbase = 0, agg = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) {
+      const uint32_t v = s_warp[i];
+      wbase += (i < warp) ? v : 0u;
+      agg += v;
+    }
+    const uint32_t lp = run + wbase + incl - cnt;   // run-relative escape prefix
+
+    // ---- run-relative group index -------------------------------------------
+    if (nvalid > 0) {
+      if (gsl >= 4) {
+        if ((base & ((int64_t(1) << gsl) - 1)) == 0) gi[base >> gsl] = lp;
+      } else {
+        const int gs = 1 << gsl;
+        for (int j = 0; j < kEPT && j < nvalid; j += gs)
+          gi[(base + j) >> gsl] = lp + __popc(esc & ((1u << j) - 1u));
+      }
+    }
+    // ---- escapes -> this run's scratch (codec.py:283-284) ---------------------
+    if (esc) {
+      uint8_t* dst = esc_out + lp;
+      uint32_t m = esc;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t word = from_smem ? tw[tid * kEPT + j] : (uint32_t)xs[base + j];
+        *dst++ = (uint8_t)((word >> 7) & 0xFFu);
+      }
+    }
+    run += agg;
+    __syncthreads();                                      // (C) stage + s_warp free
+    if (tid == 0 && t + kStages < t_end) {
+      fence_proxy_async();
+      encode_issue(xs, n, t + kStages, ring + st * kStageBytes, bars + st);
     }
   }
-  // ---- escapes out (dynamic section) ---------------------------------------
-  {
-    uint8_t* dst = frame + L.off[5] + excl;
-    for (uint32_t i = tid; i < agg; i += kThreads) dst[i] = s_esc[i];
+  if (tid == 0) run_total[blockIdx.x] = run;
+}
+
+// Pass 2: one CTA per pass-1 run.
+__global__ void __launch_bounds__(kThreads)
+encode_fixup_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __restrict__ book,
+                    uint8_t* __restrict__ frames, const uint8_t* __restrict__ scratch,
+                    const uint64_t* __restrict__ run_total, uint64_t* __restrict__ frame_len) {
+  __shared__ uint64_t s_red[kWarps];
+  __shared__ uint64_t s_off, s_zc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int seg;
+  int64_t t_begin, t_end;
+  run_range(segs, rp, blockIdx.x, seg, t_begin, t_end);
+  const int r0 = rp.run_start[seg], r1 = rp.run_start[seg + 1];
+  const bool last_run = (int)blockIdx.x == r1 - 1;
+  // offset of this run = sum of the totals of the earlier runs of the segment
+  uint64_t before = 0, all = 0;
+  for (int r = r0 + tid; r < r1; r += kThreads) {
+    const uint64_t v = run_total[r];
+    if (r < (int)blockIdx.x) before += v;
+    all += v;
   }
-  // ---- last tile of the segment: header, pads, frame length ---------------
-  const int64_t ntiles_seg = segs.tile_start[seg + 1] - segs.tile_start[seg];
-  if (t_local == ntiles_seg - 1) {
-    const uint64_t zc = excl + agg;
-    write_header_and_pads(frame, L, zc, s_book);
-    if (tid == 0) frame_len[seg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    before += __shfl_xor_sync(0xffffffffu, before, o);
+    all += __shfl_xor_sync(0xffffffffu, all, o);
   }
+  if (lane == 0) s_red[warp] = before;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t b = 0;
+    for (int i = 0; i < kWarps; ++i) b += s_red[i];
+    s_off = b;
+  }
+  __syncthreads();
+  if (lane == 0) s_red[warp] = all;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t a = 0;
+    for (int i = 0; i < kWarps; ++i) a += s_red[i];
+    s_zc = a;
+  }
+  __syncthreads();
+  const uint64_t P = s_off;
+  const int64_t n = segs.n[seg];
+  const int gsl = segs.gs_log2;
+  const Layout L = layout_of(n, gsl);
+  uint8_t* frame = frames + segs.frame_off[seg];
+  if (t_begin < t_end) {
+    // group_index: add the run offset to every group starting inside the run
+    const int64_t e0 = t_begin * kTile;
+    const int64_t e1 = (t_end * kTile < n) ? t_end * kTile : n;
+    const int64_t g0 = (e0 + (int64_t(1) << gsl) - 1) >> gsl;
+    const int64_t g1 = (e1 + (int64_t(1) << gsl) - 1) >> gsl;
+    uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
+    for (int64_t g = g0 + tid; g < g1; g += kThreads) gi[g] += (uint32_t)P;
+    // escapes: scratch run -> dynamic section at P
+    const uint64_t cnt = run_total[blockIdx.x];
+    const uint8_t* src = scratch + (segs.tile_start[seg] + t_begin) * kTile;
+    uint8_t* dst = frame + L.off[5] + P;
+    // align the destination to 4 B, then move words assembled from bytes
+    const uint32_t head = (uint32_t)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
+    const uint64_t h = cnt < head ? cnt : head;
+    if (tid < h) dst[tid] = src[tid];
+    const uint64_t body = (cnt - h) / 4;
+    uint32_t* dst4 = reinterpret_cast<uint32_t*>(dst + h);
+    for (uint64_t i = tid; i < body; i += kThreads) {
+      const uint8_t* q = src + h + 4 * i;
+      dst4[i] = (uint32_t)q[0] | (uint32_t)q[1] << 8 | (uint32_t)q[2] << 16 | (uint32_t)q[3] << 24;
+    }
+    for (uint64_t i = h + 4 * body + tid; i < cnt; i += kThreads) dst[i] = src[i];
+  }
+  if (last_run) {
+    const uint64_t zc = s_zc;
+    const int t = tid;
+    if (t < 128) {
+      uint8_t v = 0;
+      if (t < 4) v = "ZCCL"[t];
+      else if (t == 4) v = 1;
+      else if (t == 6) v = (uint8_t)gsl;
+      else if (t >= 8 && t < 16) v = (uint8_t)(uint64_t(n) >> (8 * (t - 8)));
+      else if (t >= 16 && t < 24) v = (uint8_t)(zc >> (8 * (t - 16)));
+      else if (t >= 24 && t < 31) v = book[t - 24];
+      else if (t == 31) v = book[0];
+      else if (t >= 32 && t < 56) {
+        const int i = (t - 32) >> 2;
+        int64_t o = 0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) o = (k == i) ? L.off[k] : o;
+        v = (uint8_t)(uint32_t(o) >> (8 * ((t - 32) & 3)));
+      }
+      frame[t] = v;
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      const int64_t end = r == 0 ? L.off[0] + n
+                        : r < 4 ? L.off[r] + L.plane_bytes
+                        : r == 4 ? L.off[4] + 4 * L.groups
+                                 : L.off[5] + (int64_t)zc;
+      const int64_t lim = r < 5 ? L.off[r + 1] : L.off[5] + pad128((int64_t)zc);
+      const int64_t p = end + t;
+      if (p < lim) frame[p] = 0;
+    }
+    if (t == 0) frame_len[seg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
+  }
+}
+
+// Single-pass look-back path below this many tiles (latency wins), the
+// two-kernel path above it (bandwidth wins).
+constexpr int64_t kLookbackMaxTiles = 256;
+
+static int grid_for(const void* fn, int threads, size_t dyn_smem) {
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, dyn_smem);
+  return sms * (occ > 0 ? occ : 1);
+}
+
+int64_t encode_workspace_bytes(int64_t ntiles) {
+  return 256 + 8 * 4096 + (int64_t)kTile * ntiles;
 }
 
 cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8_t* book,
                           uint8_t* frames, void* ws, uint64_t* frame_len, cudaStream_t st) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
-  unsigned* counter = reinterpret_cast<unsigned*>(ws);
-  uint64_t* status = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + 128);
-  cudaError_t e = cudaMemsetAsync(ws, 0, 128 + 8 * ntiles, st);
-  if (e != cudaSuccess) return e;
-  encode_kernel<<<(unsigned)ntiles, kThreads, 0, st>>>(x, segs, book, frames, status, counter,
-                                                      frame_len);
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
+  if (ntiles <= kLookbackMaxTiles) {
+    unsigned* counter = reinterpret_cast<unsigned*>(w8);
+    uint64_t* status = reinterpret_cast<uint64_t*>(w8 + 128);
+    cudaError_t e = cudaMemsetAsync(ws, 0, 128 + 8 * ntiles, st);
+    if (e != cudaSuccess) return e;
+    static int cap = 0;
+    if (cap == 0) cap = grid_for((const void*)encode_lookback_kernel, kThreads, 0);
+    const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    encode_lookback_kernel<<<grid, kThreads, 0, st>>>(x, segs, book, frames, status, counter,
+                                                       frame_len);
+    return cudaGetLastError();
+  }
+  const size_t dyn = kStages * kStageBytes + kStages * sizeof(uint64_t);
+  static int cap1 = 0;
+  if (cap1 == 0) {
+    cudaFuncSetAttribute(encode_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cap1 = grid_for((const void*)encode_tiles_kernel, kThreads, dyn);
+    if (cap1 > 4096) cap1 = 4096;
+  }
+  // split the resident CTAs over segments in proportion to their tiles
+  RunPlan rp{};
+  int runs = 0;
+  for (int s = 0; s < segs.nseg; ++s) {
+    const int64_t tiles = segs.tile_start[s + 1] - segs.tile_start[s];
+    int64_t want = (tiles * cap1 + ntiles - 1) / ntiles;
+    if (want < 1) want = 1;
+    if (want > tiles) want = tiles;
+    rp.run_start[s] = runs;
+    rp.tiles_per_run[s] = (tiles + want - 1) / want;
+    runs += (int)((tiles + rp.tiles_per_run[s] - 1) / rp.tiles_per_run[s]);
+  }
+  rp.run_start[segs.nseg] = runs;
+  rp.nruns = runs;
+  if (runs > 4096) return cudaErrorInvalidValue;
+  uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
+  uint8_t* scratch = w8 + 256 + 8 * 4096;
+  encode_tiles_kernel<<<runs, kThreads, dyn, st>>>(x, segs, rp, book, frames, scratch, run_total);
+  encode_fixup_kernel<<<runs, kThreads, 0, st>>>(segs, rp, book, frames, scratch, run_total,
+                                                 frame_len);
   return cudaGetLastError();
 }
 

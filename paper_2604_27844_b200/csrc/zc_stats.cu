@@ -47,86 +47,121 @@ __device__ __forceinline__ void chan_merge(double& na, double& ma, double& m2a, 
   na = n;
 }
 
+// Persistent: each CTA strides over tiles, each thread keeps running f64
+// sums of d = x - K (K = the first finite value the thread sees; non-finite
+// words are replaced by K so they add exactly 0) and the per-thread
+// (count, mean, M2) are Chan-merged once per CTA at the end.
+__device__ __forceinline__ void chan_shfl(double& n, double& m, double& q, int o) {
+  const double nb = __shfl_xor_sync(0xffffffffu, n, o);
+  const double mb = __shfl_xor_sync(0xffffffffu, m, o);
+  const double qb = __shfl_xor_sync(0xffffffffu, q, o);
+  chan_merge(n, m, q, nb, mb, qb);
+}
+
 __global__ void __launch_bounds__(kThreads)
 stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, Partial* __restrict__ out) {
   __shared__ double s_n[kWarps], s_m[kWarps], s_q[kWarps];
   __shared__ int s_e[kWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t tile = blockIdx.x;
-  const int seg = find_seg(segs.tile_start, segs.nseg, tile);
-  const int64_t n = segs.n[seg];
-  const uint16_t* xs = x + segs.x_off[seg];
-  const int64_t base = (tile - segs.tile_start[seg]) * kTile + (int64_t)tid * kEPT;
-  const int64_t nvalid = n - base;
+  const int64_t ntiles = segs.tile_start[segs.nseg];
 
-  uint32_t w[8];
-  if (nvalid >= kEPT && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)) {
-    uint4 a = ld_stream_v4(xs + base), b = ld_stream_v4(xs + base + 8);
-    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-    w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-  } else {
+  bool have_k = false;
+  uint32_t kword = 0;        // K as a bf16 word in the high half of an f32
+  double K = 0.0, s1 = 0.0, s2 = 0.0;
+  uint64_t cnt = 0;
+  int kexp = -1;
+
+  uint32_t w[8], nw[8];
+  auto load = [&](int64_t tile, uint32_t* dst) {
+    const int s = find_seg(segs.tile_start, segs.nseg, tile);
+    const uint16_t* xs = x + segs.x_off[s];
+    const int64_t base = (tile - segs.tile_start[s]) * kTile + (int64_t)tid * kEPT;
+    const int64_t nvalid = segs.n[s] - base;
+    if (nvalid >= kEPT && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)) {
+      const uint4 a = ld_stream_v4(xs + base), b = ld_stream_v4(xs + base + 8);
+      dst[0] = a.x; dst[1] = a.y; dst[2] = a.z; dst[3] = a.w;
+      dst[4] = b.x; dst[5] = b.y; dst[6] = b.z; dst[7] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        // out-of-range elements become NaN words: excluded like non-finite
+        const uint32_t lo = (2 * k < nvalid) ? xs[base + 2 * k] : 0x7FC0u;
+        const uint32_t hi = (2 * k + 1 < nvalid) ? xs[base + 2 * k + 1] : 0x7FC0u;
+        dst[k] = lo | (hi << 16);
+      }
+    }
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) load(tile, w);
+  while (tile < ntiles) {
+    const int64_t nt = tile + gridDim.x;
+    if (nt < ntiles) load(nt, nw);
+    // finite test per half: exponent field != 255 (bf16.py:100 np.isfinite);
+    // bit 15 / bit 31 of v set iff the low / high word is finite
+    uint32_t v[8], allfin = 0x80008000u;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      // out-of-range elements become NaN words (0x7FC0): excluded like non-finite
-      uint32_t lo = (2 * k < nvalid) ? xs[base + 2 * k] : 0x7FC0u;
-      uint32_t hi = (2 * k + 1 < nvalid) ? xs[base + 2 * k + 1] : 0x7FC0u;
-      w[k] = lo | (hi << 16);
+      v[k] = (~w[k] & 0x7F807F80u) + 0x7F807F80u;
+      allfin &= v[k];
     }
-  }
-  // finite mask: exponent field != 255 (bf16.py:100 np.isfinite)
-  uint32_t fin = 0;
+    if (allfin == 0x80008000u && have_k) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    fin |= (((w[k] & 0x7F80u) != 0x7F80u) ? 1u : 0u) << (2 * k);
-    fin |= (((w[k] & 0x7F800000u) != 0x7F800000u) ? 1u : 0u) << (2 * k + 1);
-  }
-  // warp shift K = first finite element of the warp
-  const unsigned any = __ballot_sync(0xffffffffu, fin != 0);
-  double K = 0.0;
-  int kexp = -1;
-  if (any) {
-    const int src = __ffs(any) - 1;
-    uint32_t word = 0;
-    if (lane == src) {
-      const int k = __ffs(fin) - 1;
-      word = (k & 1) ? (w[k >> 1] >> 16) : (w[k >> 1] & 0xFFFFu);
+      for (int k = 0; k < 8; ++k) {
+        const double lo = (double)__uint_as_float(w[k] << 16) - K;
+        const double hi = (double)__uint_as_float(w[k] & 0xFFFF0000u) - K;
+        s1 += lo;
+        s2 = fma(lo, lo, s2);
+        s1 += hi;
+        s2 = fma(hi, hi, s2);
+      }
+      cnt += kEPT;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t word = (k & 1) ? (w[k >> 1] >> 16) : (w[k >> 1] & 0xFFFFu);
+        const bool fin = (v[k >> 1] >> ((k & 1) ? 31 : 15)) & 1u;
+        if (fin && !have_k) {
+          have_k = true;
+          kword = word;
+          K = (double)__uint_as_float(word << 16);
+          kexp = (word >> 7) & 0xFF;
+        }
+        if (fin) {
+          const double d = (double)__uint_as_float(word << 16) - K;
+          s1 += d;
+          s2 = fma(d, d, s2);
+          ++cnt;
+        }
+      }
     }
-    word = __shfl_sync(0xffffffffu, word, src);
-    K = (double)__uint_as_float(word << 16);
-    kexp = (word >> 7) & 0xFF;
-  }
-  double s1 = 0.0, s2 = 0.0;
+    tile = nt;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const uint32_t word = (k & 1) ? (w[k >> 1] & 0xFFFF0000u) : (w[k >> 1] << 16);
-    const double d = (fin >> k & 1u) ? ((double)__uint_as_float(word) - K) : 0.0;
-    s1 += d;
-    s2 = fma(d, d, s2);
+    for (int k = 0; k < 8; ++k) w[k] = nw[k];
   }
-  double c = (double)__popc(fin);
+  (void)kword;
+  // per-thread (count, mean, M2), then Chan merge: warp tree, then warps
+  double c = (double)cnt, m = 0.0, q = 0.0;
+  if (cnt > 0) {
+    m = K + s1 / c;
+    q = fmax(s2 - s1 * (s1 / c), 0.0);
+  }
+  int e = kexp;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    c += __shfl_xor_sync(0xffffffffu, c, o);
+  for (int o = 1; o < 32; o <<= 1) {
+    chan_shfl(c, m, q, o);
+    const int eb = __shfl_xor_sync(0xffffffffu, e, o);
+    e = (e < 0) ? eb : e;
   }
-  if (lane == 0) {
-    double mean = 0.0, m2 = 0.0;
-    if (c > 0.0) {
-      mean = K + s1 / c;
-      m2 = fmax(s2 - s1 * (s1 / c), 0.0);
-    }
-    s_n[warp] = c; s_m[warp] = mean; s_q[warp] = m2; s_e[warp] = kexp;
-  }
+  if (lane == 0) { s_n[warp] = c; s_m[warp] = m; s_q[warp] = q; s_e[warp] = e; }
   __syncthreads();
   if (tid == 0) {
     double na = 0.0, ma = 0.0, qa = 0.0;
-    int e = -1;
+    int ea = -1;
     for (int i = 0; i < kWarps; ++i) {
       chan_merge(na, ma, qa, s_n[i], s_m[i], s_q[i]);
-      if (e < 0) e = s_e[i];
+      if (ea < 0) ea = s_e[i];
     }
-    out[tile] = Partial{na, ma, qa, (double)e};
+    out[blockIdx.x] = Partial{na, ma, qa, (double)ea};
   }
 }
 
@@ -235,8 +270,17 @@ cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, in
                                      void* ws, uint8_t* book, double* result, cudaStream_t st) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
   Partial* parts = reinterpret_cast<Partial*>(reinterpret_cast<uint8_t*>(ws) + 128);
-  if (ntiles > 0) stats_kernel<<<(unsigned)ntiles, kThreads, 0, st>>>(x, segs, parts);
-  finalize_kernel<<<1, 1024, 0, st>>>(parts, ntiles, total, book, result);
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stats_kernel, kThreads, 0);
+    grid_cap = sms * (occ > 0 ? occ : 1);
+  }
+  const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
+  if (grid > 0) stats_kernel<<<(unsigned)grid, kThreads, 0, st>>>(x, segs, parts);
+  finalize_kernel<<<1, 1024, 0, st>>>(parts, grid, total, book, result);
   return cudaGetLastError();
 }
 

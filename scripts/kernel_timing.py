@@ -36,6 +36,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=1 << 28)
     ap.add_argument("--sigma", type=float, default=0.02)
+    ap.add_argument("--repeat", type=int, default=0)
+    ap.add_argument("--no-check", action="store_true")
     args = ap.parse_args()
     n = args.n
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -48,8 +50,17 @@ def main():
     F = int(flen.item())
     out = torch.empty_like(w)
     err = engine.decode([frames.data_ptr()], [0], None, [n], out, [0])
-    assert int(err.item()) == engine.ERR_OK
-    assert torch.equal(out, w)
+    code = int(err.item())
+    if not args.no_check:
+        assert code == engine.ERR_OK, engine.err_message(code)
+        assert torch.equal(out, w)
+    ref = frames[:F].clone()
+    for _ in range(args.repeat):   # determinism / race stress
+        engine.encode(w, [(0, n)], book, 9, frames, [0], flen)
+        e2 = engine.decode([frames.data_ptr()], [0], None, [n], out, [0])
+        c2 = int(e2.item())
+        assert c2 == engine.ERR_OK, engine.err_message(c2)
+        assert torch.equal(frames[:F], ref) and torch.equal(out, w)
     t_stats = timed(lambda: engine.measured_codebook(w))
     t_enc = timed(lambda: engine.encode(w, [(0, n)], book, 9, frames, [0], flen))
     t_dec = timed(lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0]))
