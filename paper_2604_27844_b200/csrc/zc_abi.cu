@@ -135,7 +135,7 @@ int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64
               const int64_t* n, const int64_t* out_off, int nseg, uint16_t* out, int32_t* err_dev,
               void* ws, int64_t ws_bytes, int write_out, cudaStream_t stream) {
   if (nseg < 1 || nseg > kMaxSegments || !stat || !dyn || !n || !err_dev || !ws) return kStatusBadArg;
-  if (write_out && (!out || !out_off)) return kStatusBadArg;
+  if ((write_out & 1) && (!out || !out_off)) return kStatusBadArg;
   DecodeSegs s{};
   s.nseg = nseg;
   s.tile_start[0] = 0;
@@ -150,7 +150,7 @@ int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64
     s.tile_start[i + 1] = s.tile_start[i] + tiles_of(n[i]);
   }
   if (128 + 8 * s.tile_start[nseg] > ws_bytes) return kStatusWorkspace;
-  return status_of(launch_decode(s, out, err_dev, ws, write_out, stream));
+  return status_of(launch_decode(s, out, err_dev, ws, write_out, stream));  // write_out: flags
 }
 
 }  // extern "C"

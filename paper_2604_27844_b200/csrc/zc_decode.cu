@@ -107,7 +107,7 @@ __device__ __forceinline__ void reassemble4(uint32_t S, uint32_t E, uint32_t& o0
 }
 
 __global__ void __launch_bounds__(kThreads)
-decode_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_t* __restrict__ err,
+decode_lookback_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_t* __restrict__ err,
               uint64_t* __restrict__ status, unsigned* __restrict__ counter, int write_out) {
   __shared__ uint32_t s_spread[256];
   __shared__ __align__(16) uint8_t s_dense[kTile];
@@ -331,26 +331,332 @@ decode_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_t* __rest
   }
 }
 
+// ============================================================================
+// Ring decoder (group size <= tile, i.e. every tile starts a group — always
+// the case for the collectives' 512).  Warp-specialised: warp 0 is the
+// producer, warps 1..8 decode.  Each CTA owns a contiguous run of tiles of
+// one segment.  For every tile the producer stages, with TMA bulk copies into
+// a kStages ring: the 4 KB sign-mantissa slice, the three 512 B plane slices,
+// the tile's group_index slice and the tile's escape bytes (their range is
+// [gi[first group of tile], gi[first group of next tile]) — the producer
+// warp fetches 32 tile boundaries at a time).  Consumers therefore never
+// wait on global memory: every escape is read from shared memory at its
+// tile-local rank, and consistency is checked as gi[g] == gi[tile] +
+// escapes-before-g inside the tile plus gi[tile] + tile escapes ==
+// gi[next tile] (zero_count after the last tile) — equivalent to the
+// reference's diff(gi) == per-group escapes, gi[0] == 0, sum == zero_count.
+// ============================================================================
+
+constexpr int kDStages = 4;
+constexpr int kGiSlots = 264;                       // up to 257 gi entries (gs >= 16) + align
+constexpr int kEscSlots = kTile + 32;
+struct __align__(128) DStage {
+  uint8_t sm[kTile];
+  uint8_t pl[3][kTile / 8];
+  uint32_t gi[kGiSlots];
+  uint8_t esc[kEscSlots];
+};
+constexpr int kDStageBytes = sizeof(DStage);
+constexpr int kDThreads = kThreads + 32;
+
+struct DRunPlan {
+  int nruns;
+  int run_start[kMaxSegments + 1];
+  int64_t tiles_per_run[kMaxSegments];
+};
+
+__device__ __forceinline__ uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
+
+__global__ void __launch_bounds__(kDThreads)
+decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restrict__ out,
+                   int32_t* __restrict__ err, int write_out) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  DStage* ring = reinterpret_cast<DStage*>(s_dyn);
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_dyn + kDStages * kDStageBytes);
+  uint64_t* empty = full + kDStages;
+  __shared__ __align__(16) uint32_t s_warp[2][kWarps];
+  __shared__ HeaderInfo s_hdr;
+  __shared__ int64_t s_lo[kDStages], s_al[kDStages], s_cnt[kDStages];
+  __shared__ int32_t s_gi_shift[kDStages];
+  __shared__ uint32_t s_spread[256];
+
+  const int tid = threadIdx.x;
+  if (tid >= 32) {
+    const int v = tid - 32;   // byte -> nibble spread: bit k -> bit 4k
+    uint32_t sp = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sp |= ((uint32_t(v) >> k) & 1u) << (4 * k);
+    s_spread[v] = sp;
+  }
+  // ---- this CTA's run ------------------------------------------------------
+  int seg = 0;
+  while (seg + 1 < segs.nseg && (int)blockIdx.x >= rp.run_start[seg + 1]) ++seg;
+  const int64_t seg_tiles = segs.tile_start[seg + 1] - segs.tile_start[seg];
+  int64_t t_begin = (blockIdx.x - rp.run_start[seg]) * rp.tiles_per_run[seg];
+  int64_t t_end = t_begin + rp.tiles_per_run[seg];
+  if (t_begin > seg_tiles) t_begin = seg_tiles;
+  if (t_end > seg_tiles) t_end = seg_tiles;
+  const uint8_t* frame = segs.stat[seg];
+
+  if (tid == 0) {
+    s_hdr = check_header(frame, segs.n[seg], segs.dyn_len[seg]);
+    for (int i = 0; i < kDStages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const HeaderInfo H = s_hdr;
+  if (H.err != kOk) {
+    if (tid == 0) atomicMin(err + seg, H.err);
+    return;
+  }
+  const int64_t n = H.n;
+  const int gsl = H.gsl;
+  const Layout L = layout_of(n, gsl);
+  const uint8_t* dyn = segs.dyn[seg] ? segs.dyn[seg] : frame + L.off[5];
+  const uint32_t* gi = reinterpret_cast<const uint32_t*>(frame + L.off[4]);
+  const int64_t gpt = int64_t(kTile) >> gsl;          // groups per full tile
+  const bool stage_gi = gsl >= 4;                     // slice fits kGiSlots
+
+  if (tid < 32) {
+    // ======================= producer warp ===============================
+    const int lane = tid;
+    const int64_t zcap = pad128(H.zc);
+    for (int64_t c0 = t_begin; c0 < t_end; c0 += 32) {
+      // escape-range bounds of 32 tiles at once: bound(t) = gi[first group of t]
+      const int64_t tb = c0 + lane;
+      int64_t bnd = H.zc;
+      if (tb < seg_tiles) bnd = (int64_t)gi[tb * gpt];
+      const int64_t tb2 = c0 + 32;
+      const int64_t bnd32 = (tb2 < seg_tiles) ? (int64_t)gi[tb2 * gpt] : H.zc;
+      for (int j = 0; j < 32 && c0 + j < t_end; ++j) {
+        const int64_t lo = __shfl_sync(0xffffffffu, bnd, j);
+        const int64_t hi = (j < 31) ? __shfl_sync(0xffffffffu, bnd, j + 1) : bnd32;
+        if (lane == 0) {
+          const int64_t t = c0 + j, k = t - t_begin;
+          const int st = (int)(k % kDStages);
+          if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
+          DStage& S = ring[st];
+          const int64_t e0 = t * kTile;
+          const int64_t valid = (n - e0) < kTile ? (n - e0) : kTile;
+          const uint32_t b_sm = r16(valid), b_pl = r16((valid + 7) >> 3);
+          // escapes: clamp into the section so a corrupt index stays memory-safe
+          int64_t clo = lo < 0 ? 0 : (lo > H.zc ? H.zc : lo);
+          int64_t chi = hi < clo ? clo : (hi > H.zc ? H.zc : hi);
+          const uint8_t* esrc = dyn + clo;
+          const uint8_t* eal = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(esrc) & ~uintptr_t(15));
+          int64_t eb = (int64_t)r16((uint64_t)(chi - clo) + (uint64_t)(esrc - eal));
+          if (eb > kEscSlots) eb = kEscSlots;
+          if ((eal - dyn) + eb > zcap + 128) eb = 0;   // never read past the padded section
+          // group_index slice [g0, g0 + ng] (+1 for the next tile's first entry)
+          uint32_t b_gi = 0;
+          const uint32_t* gsrc = gi;
+          int32_t shift = 0;
+          if (stage_gi) {
+            const int64_t g0 = t * gpt;
+            int64_t ng = (valid + (int64_t(1) << gsl) - 1) >> gsl;
+            if (g0 + ng < L.groups) ng += 1;
+            const uint32_t* gp = gi + g0;
+            gsrc = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
+            shift = (int32_t)(gp - gsrc);
+            b_gi = r16((uint64_t)(ng + shift) * 4);
+          }
+          s_lo[st] = clo;
+          s_al[st] = eal - dyn;
+          s_cnt[st] = chi - clo;
+          s_gi_shift[st] = shift;
+          mbar_arrive_expect_tx(full + st, b_sm + 3 * b_pl + b_gi + (uint32_t)eb);
+          tma_load_1d(S.sm, frame + L.off[0] + e0, b_sm, full + st);
+          for (int b = 0; b < 3; ++b)
+            tma_load_1d(S.pl[b], frame + L.off[1 + b] + (e0 >> 3), b_pl, full + st);
+          if (b_gi) tma_load_1d(S.gi, gsrc, b_gi, full + st);
+          if (eb) tma_load_1d(S.esc, eal, (uint32_t)eb, full + st);
+        }
+      }
+    }
+    return;
+  }
+
+  // ========================= consumer warps ==============================
+  const int ct = tid - 32, lane = ct & 31, warp = ct >> 5;
+  int32_t my_err = kOk;
+  const int64_t seg_t0 = segs.tile_start[seg];
+  (void)seg_t0;
+  for (int64_t t = t_begin; t < t_end; ++t) {
+    const int64_t k = t - t_begin;
+    const int st = (int)(k % kDStages);
+    mbar_wait(full + st, (uint32_t)((k / kDStages) & 1));
+    const DStage& S = ring[st];
+    const int64_t tile_base = t * kTile;
+    const int64_t base = tile_base + (int64_t)ct * kEPT;
+    const int64_t nvalid = n - base;
+    const bool full_t = nvalid >= kEPT;
+    const uint32_t valid16 = full_t ? 0xFFFFu : (nvalid > 0 ? ((1u << nvalid) - 1u) : 0u);
+
+    uint4 sv = make_uint4(0, 0, 0, 0);
+    uint32_t p0 = 0, p1 = 0, p2 = 0;
+    if (nvalid > 0) {
+      sv = *reinterpret_cast<const uint4*>(S.sm + ct * kEPT);
+      p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + ct * 2);
+      p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + ct * 2);
+      p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
+    }
+    const uint32_t esc = ~(p0 | p1 | p2) & valid16;
+
+    // ---- tile-local scan -----------------------------------------------------
+    const uint32_t cnt = __popc(esc);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    uint32_t* sw = s_warp[k & 1];
+    if (lane == 31) sw[warp] = incl;
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+    uint32_t wbase = 0, agg = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) {
+      const uint32_t v = sw[i];
+      wbase += (i < warp) ? v : 0u;
+      agg += v;
+    }
+    const uint32_t lp = wbase + incl - cnt;
+    const int64_t lo = s_lo[st];
+    const int64_t tcnt = s_cnt[st];
+
+    // ---- consistency (codec.py:238-250) --------------------------------------
+    if (nvalid > 0) {
+      auto gi_at = [&](int64_t g) -> int64_t {
+        if (stage_gi) return (int64_t)S.gi[s_gi_shift[st] + (g - t * gpt)];
+        return (int64_t)gi[g];
+      };
+      if (gsl >= 4) {
+        if ((base & ((int64_t(1) << gsl) - 1)) == 0) {
+          const int64_t g = base >> gsl;
+          if (gi_at(g) != lo + (int64_t)lp) my_err = kErrGroupIndex;
+        }
+      } else {
+        const int gs = 1 << gsl;
+        for (int j = 0; j < kEPT && j < nvalid; j += gs) {
+          const int64_t g = (base + j) >> gsl;
+          if ((int64_t)gi[g] != lo + (int64_t)lp + __popc(esc & ((1u << j) - 1u))) my_err = kErrGroupIndex;
+        }
+      }
+      if (ct == 0) {
+        if (t == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
+        // tile end: next tile's first entry, or zero_count after the last tile
+        if ((int64_t)agg != tcnt) my_err = (t + 1 < seg_tiles) ? kErrGroupIndex : kErrZeroCount;
+      }
+    }
+
+    // ---- exponents: codes -> PRMT table lookup ------------------------------
+    uint32_t E[4];
+    {
+      const uint32_t lo8 = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
+      const uint32_t hi8 = s_spread[(p0 >> 8) & 0xFF] | s_spread[(p1 >> 8) & 0xFF] << 1 |
+                           s_spread[(p2 >> 8) & 0xFF] << 2;
+      E[0] = prmt(H.tbl_lo, H.tbl_hi, lo8);
+      E[1] = prmt(H.tbl_lo, H.tbl_hi, lo8 >> 16);
+      E[2] = prmt(H.tbl_lo, H.tbl_hi, hi8);
+      E[3] = prmt(H.tbl_lo, H.tbl_hi, hi8 >> 16);
+    }
+    // ---- escapes from the staged bytes at their tile-local rank -------------
+    if (esc) {
+      const uint8_t* eb = S.esc + (lo - s_al[st]);
+      uint32_t m = esc;
+      uint32_t r = lp;
+      uint32_t ins[4] = {0, 0, 0, 0};
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        uint32_t v = 0;
+        if ((int64_t)r < tcnt) v = eb[r];
+        else my_err = kErrZeroCount;   // always accompanied by a failing index check
+        ++r;
+        const uint32_t sh = 8 * (j & 3);
+        const int q = j >> 2;
+        ins[0] |= (q == 0) ? v << sh : 0u;
+        ins[1] |= (q == 1) ? v << sh : 0u;
+        ins[2] |= (q == 2) ? v << sh : 0u;
+        ins[3] |= (q == 3) ? v << sh : 0u;
+      }
+      E[0] |= ins[0]; E[1] |= ins[1]; E[2] |= ins[2]; E[3] |= ins[3];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+
+    // ---- reassemble (codec.py:308-312) and store ---------------------------
+    if (write_out && nvalid > 0) {
+      uint32_t o[8];
+      reassemble4(sv.x, E[0], o[0], o[1]);
+      reassemble4(sv.y, E[1], o[2], o[3]);
+      reassemble4(sv.z, E[2], o[4], o[5]);
+      reassemble4(sv.w, E[3], o[6], o[7]);
+      uint16_t* dst = out + segs.out_off[seg] + base;
+      if (full_t && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        st_stream_v4(dst, make_uint4(o[0], o[1], o[2], o[3]));
+        st_stream_v4(dst + 8, make_uint4(o[4], o[5], o[6], o[7]));
+      } else {
+        const int lim = full_t ? kEPT : (int)nvalid;
+        for (int j = 0; j < lim; ++j) dst[j] = (uint16_t)(o[j >> 1] >> (16 * (j & 1)));
+      }
+    }
+  }
+  if (my_err != kOk) atomicMin(err + seg, my_err);
+}
+
+static int grid_cap(const void* fn, int threads, size_t dyn) {
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, dyn);
+  return sms * (occ > 0 ? occ : 1);
+}
+
 cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, void* ws,
-                          int write_out, cudaStream_t st) {
+                          int flags, cudaStream_t st) {
+  // flags bit 0: write the words; bit 1: frames may use groups larger than a
+  // tile (then the look-back decoder is used)
+  const int write_out = flags & 1;
+  const int any_large_groups = (flags >> 1) & 1;
   const int64_t ntiles = segs.tile_start[segs.nseg];
-  unsigned* counter = reinterpret_cast<unsigned*>(ws);
-  uint64_t* status = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + 128);
-  cudaError_t e = cudaMemsetAsync(ws, 0, 128 + 8 * ntiles, st);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(err, 0x7F, sizeof(int32_t) * segs.nseg, st);
+  cudaError_t e = cudaMemsetAsync(err, 0x7F, sizeof(int32_t) * segs.nseg, st);
   if (e != cudaSuccess) return e;
   if (ntiles == 0) return cudaSuccess;
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel, kThreads, 0);
-    grid_cap = sms * (occ > 0 ? occ : 1);
+  if (any_large_groups) {
+    unsigned* counter = reinterpret_cast<unsigned*>(ws);
+    uint64_t* status = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + 128);
+    e = cudaMemsetAsync(ws, 0, 128 + 8 * ntiles, st);
+    if (e != cudaSuccess) return e;
+    static int cap = 0;
+    if (cap == 0) cap = grid_cap((const void*)decode_lookback_kernel, kThreads, 0);
+    const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    decode_lookback_kernel<<<grid, kThreads, 0, st>>>(segs, out, err, status, counter, write_out);
+    return cudaGetLastError();
   }
-  const unsigned grid = (unsigned)(ntiles < grid_cap ? ntiles : grid_cap);
-  decode_kernel<<<grid, kThreads, 0, st>>>(segs, out, err, status, counter, write_out);
+  const size_t dyn = kDStages * kDStageBytes + 2 * kDStages * sizeof(uint64_t);
+  static int cap2 = 0;
+  if (cap2 == 0) {
+    cudaFuncSetAttribute(decode_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cap2 = grid_cap((const void*)decode_ring_kernel, kDThreads, dyn);
+  }
+  DRunPlan rp{};
+  int runs = 0;
+  for (int s = 0; s < segs.nseg; ++s) {
+    const int64_t tiles = segs.tile_start[s + 1] - segs.tile_start[s];
+    int64_t want = (tiles * cap2 + ntiles - 1) / ntiles;
+    if (want < 1) want = 1;
+    if (want > tiles) want = tiles;
+    rp.run_start[s] = runs;
+    rp.tiles_per_run[s] = (tiles + want - 1) / want;
+    runs += (int)((tiles + rp.tiles_per_run[s] - 1) / rp.tiles_per_run[s]);
+  }
+  rp.run_start[segs.nseg] = runs;
+  rp.nruns = runs;
+  decode_ring_kernel<<<runs, kDThreads, dyn, st>>>(segs, rp, out, err, write_out);
   return cudaGetLastError();
 }
 

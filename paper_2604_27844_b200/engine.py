@@ -15,6 +15,7 @@ from . import _lib
 from ._lib import check, i64s, lib, ptrs, stream_ptr
 
 WORD = torch.int16
+TILE = _lib.TILE
 
 
 def words_view(t: torch.Tensor) -> torch.Tensor:
@@ -111,13 +112,15 @@ def encode(words: torch.Tensor, segs, book: torch.Tensor, gs_log2: int,
 
 def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_offs,
            write_out: bool = True, err: torch.Tensor | None = None, stream=None,
-           device=None) -> torch.Tensor:
+           device=None, large_groups: bool = False) -> torch.Tensor:
     """K3/K5: decode (and validate) one frame per segment.
 
     stat_ptrs/dyn_ptrs are raw device addresses (local or peer-mapped);
     dyn_ptrs entries may be 0 for "dynamic section in place".  Returns the
-    int32[nseg] device error words (0x7F7F7F7F = ok).
+    int32[nseg] device error words (0x7F7F7F7F = ok).  ``large_groups``
+    must be set when a frame may use groups larger than 4096 elements.
     """
+    flags = (1 if write_out else 0) | (2 if large_groups else 0)
     nseg = len(counts)
     dev = out.device if out is not None else torch.device(device or "cuda")
     if err is None:
@@ -131,7 +134,7 @@ def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_
             i64s(dyn_lens[lo:hi]) if dyn_lens is not None else None,
             i64s(counts[lo:hi]), i64s(out_offs[lo:hi]) if out_offs is not None else None,
             len(counts[lo:hi]), out.data_ptr() if out is not None else None,
-            err.data_ptr() + 4 * lo, ws.data_ptr(), ws.numel(), 1 if write_out else 0,
+            err.data_ptr() + 4 * lo, ws.data_ptr(), ws.numel(), flags,
             stream_ptr(stream)), "zc_decode")
     return err
 
