@@ -379,6 +379,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
   __shared__ int64_t s_lo[kDStages], s_al[kDStages], s_cnt[kDStages];
   __shared__ int32_t s_gi_shift[kDStages];
   __shared__ uint32_t s_spread[256];
+  __shared__ __align__(16) uint8_t s_slot[kThreads * kEPT];
 
   const int tid = threadIdx.x;
   if (tid >= 32) {
@@ -480,10 +481,13 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
   }
 
   // ========================= consumer warps ==============================
+  // Mode A (gs <= 512): a warp's 512 elements start a group, so its escape
+  // base is gi[first group of the warp] — warps are independent, no block
+  // scan.  Mode B (1024 <= gs <= 4096): groups span warps; block scan.
   const int ct = tid - 32, lane = ct & 31, warp = ct >> 5;
+  const bool modeA = gsl <= 9;
+  uint8_t* slot = s_slot + ct * kEPT;
   int32_t my_err = kOk;
-  const int64_t seg_t0 = segs.tile_start[seg];
-  (void)seg_t0;
   for (int64_t t = t_begin; t < t_end; ++t) {
     const int64_t k = t - t_begin;
     const int st = (int)(k % kDStages);
@@ -491,117 +495,138 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     const DStage& S = ring[st];
     const int64_t tile_base = t * kTile;
     const int64_t base = tile_base + (int64_t)ct * kEPT;
-    const int64_t nvalid = n - base;
-    const bool full_t = nvalid >= kEPT;
-    const uint32_t valid16 = full_t ? 0xFFFFu : (nvalid > 0 ? ((1u << nvalid) - 1u) : 0u);
+    const int nv = (int)((n - base) < kEPT ? (n - base) : kEPT);   // may be <= 0
+    const uint32_t valid16 = nv >= kEPT ? 0xFFFFu : (nv > 0 ? ((1u << nv) - 1u) : 0u);
+    const int64_t lo = s_lo[st];
+    const int32_t tcnt = (int32_t)s_cnt[st];
+    const int32_t esc_off = (int32_t)(lo - s_al[st]);
+    const int gshift = s_gi_shift[st];
+    const int64_t g0 = t * gpt;
+    auto gi_at = [&](int64_t g) -> int64_t {   // g within this tile, or its first successor
+      if (g >= L.groups) return H.zc;
+      if (stage_gi) return (int64_t)S.gi[gshift + (int)(g - g0)];
+      return (int64_t)gi[g];
+    };
 
     uint4 sv = make_uint4(0, 0, 0, 0);
     uint32_t p0 = 0, p1 = 0, p2 = 0;
-    if (nvalid > 0) {
+    if (nv > 0) {
       sv = *reinterpret_cast<const uint4*>(S.sm + ct * kEPT);
       p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + ct * 2);
       p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + ct * 2);
       p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
     }
     const uint32_t esc = ~(p0 | p1 | p2) & valid16;
-
-    // ---- tile-local scan -----------------------------------------------------
     const uint32_t cnt = __popc(esc);
     uint32_t incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+      incl += (lane >= o) ? v : 0u;
     }
-    uint32_t* sw = s_warp[k & 1];
-    if (lane == 31) sw[warp] = incl;
-    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
-    uint32_t wbase = 0, agg = 0;
-#pragma unroll
-    for (int i = 0; i < kWarps; ++i) {
-      const uint32_t v = sw[i];
-      wbase += (i < warp) ? v : 0u;
-      agg += v;
-    }
-    const uint32_t lp = wbase + incl - cnt;
-    const int64_t lo = s_lo[st];
-    const int64_t tcnt = s_cnt[st];
-
-    // ---- consistency (codec.py:238-250) --------------------------------------
-    if (nvalid > 0) {
-      auto gi_at = [&](int64_t g) -> int64_t {
-        if (stage_gi) return (int64_t)S.gi[s_gi_shift[st] + (g - t * gpt)];
-        return (int64_t)gi[g];
-      };
-      if (gsl >= 4) {
-        if ((base & ((int64_t(1) << gsl) - 1)) == 0) {
-          const int64_t g = base >> gsl;
-          if (gi_at(g) != lo + (int64_t)lp) my_err = kErrGroupIndex;
-        }
-      } else {
-        const int gs = 1 << gsl;
-        for (int j = 0; j < kEPT && j < nvalid; j += gs) {
-          const int64_t g = (base + j) >> gsl;
-          if ((int64_t)gi[g] != lo + (int64_t)lp + __popc(esc & ((1u << j) - 1u))) my_err = kErrGroupIndex;
+    const uint32_t wexcl = incl - cnt;               // escapes in the warp before me
+    int32_t rank0;                                   // tile-local rank of my first escape
+    if (modeA) {
+      const int64_t gw = (tile_base + warp * 512) >> gsl;     // warp's first group
+      const bool warp_live = tile_base + warp * 512 < n;
+      const int32_t wbase = warp_live ? (int32_t)(gi_at(gw) - lo) : 0;
+      rank0 = wbase + (int32_t)wexcl;
+      const int tpg = gsl >= 4 ? 1 << (gsl - 4) : 1;          // threads per group
+      const uint32_t gend = __shfl_sync(0xffffffffu, incl, (lane | (tpg - 1)) & 31);
+      if (nv > 0) {
+        if (gsl >= 4) {
+          if ((lane & (tpg - 1)) == 0) {
+            const int64_t g = base >> gsl;
+            const int64_t c = (int64_t)(gend - wexcl);
+            const int64_t gv = lo + rank0;           // == gi[g] when consistent
+            if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
+            if (gi_at(g) != gv || gv + c != gi_at(g + 1))
+              my_err = (g + 1 < L.groups) ? kErrGroupIndex : kErrZeroCount;
+          }
+        } else {
+          const int gs = 1 << gsl;
+          int32_t r = rank0;
+          for (int j = 0; j < kEPT && j < nv; j += gs) {
+            const int64_t g = (base + j) >> gsl;
+            const int64_t c = __popc(esc & (((1u << gs) - 1u) << j));
+            if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
+            if (gi_at(g) != lo + r || lo + r + c != gi_at(g + 1))
+              my_err = (g + 1 < L.groups) ? kErrGroupIndex : kErrZeroCount;
+            r += (int32_t)c;
+          }
         }
       }
+    } else {
+      uint32_t* sw = s_warp[k & 1];
+      if (lane == 31) sw[warp] = incl;
+      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+      uint32_t v = lane < kWarps ? sw[lane] : 0u, vi = v;
+#pragma unroll
+      for (int o = 1; o < kWarps; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, vi, o);
+        vi += (lane >= o) ? u : 0u;
+      }
+      const uint32_t wb = __shfl_sync(0xffffffffu, vi - v, warp);
+      rank0 = (int32_t)(wb + wexcl);
+      if (nv > 0 && (base & ((int64_t(1) << gsl) - 1)) == 0) {
+        const int64_t g = base >> gsl;
+        if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
+        if (gi_at(g) != lo + rank0) my_err = kErrGroupIndex;
+      }
+      const uint32_t agg = __shfl_sync(0xffffffffu, vi, kWarps - 1);
       if (ct == 0) {
-        if (t == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
-        // tile end: next tile's first entry, or zero_count after the last tile
-        if ((int64_t)agg != tcnt) my_err = (t + 1 < seg_tiles) ? kErrGroupIndex : kErrZeroCount;
+        if ((int32_t)agg != tcnt) my_err = (g0 + gpt < L.groups) ? kErrGroupIndex : kErrZeroCount;
       }
     }
 
     // ---- exponents: codes -> PRMT table lookup ------------------------------
-    uint32_t E[4];
+    uint32_t E0, E1, E2, E3;
     {
       const uint32_t lo8 = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
       const uint32_t hi8 = s_spread[(p0 >> 8) & 0xFF] | s_spread[(p1 >> 8) & 0xFF] << 1 |
                            s_spread[(p2 >> 8) & 0xFF] << 2;
-      E[0] = prmt(H.tbl_lo, H.tbl_hi, lo8);
-      E[1] = prmt(H.tbl_lo, H.tbl_hi, lo8 >> 16);
-      E[2] = prmt(H.tbl_lo, H.tbl_hi, hi8);
-      E[3] = prmt(H.tbl_lo, H.tbl_hi, hi8 >> 16);
+      E0 = prmt(H.tbl_lo, H.tbl_hi, lo8);
+      E1 = prmt(H.tbl_lo, H.tbl_hi, lo8 >> 16);
+      E2 = prmt(H.tbl_lo, H.tbl_hi, hi8);
+      E3 = prmt(H.tbl_lo, H.tbl_hi, hi8 >> 16);
     }
-    // ---- escapes from the staged bytes at their tile-local rank -------------
+    // ---- escapes: staged bytes at their tile-local rank -> per-thread slot ---
     if (esc) {
-      const uint8_t* eb = S.esc + (lo - s_al[st]);
+      *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
+      const uint8_t* eb = S.esc + esc_off;
       uint32_t m = esc;
-      uint32_t r = lp;
-      uint32_t ins[4] = {0, 0, 0, 0};
+      int32_t r = rank0;
       while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1;
-        uint32_t v = 0;
-        if ((int64_t)r < tcnt) v = eb[r];
+        uint8_t v = 0;
+        if ((uint32_t)r < (uint32_t)tcnt) v = eb[r];
         else my_err = kErrZeroCount;   // always accompanied by a failing index check
+        slot[j] = v;
         ++r;
-        const uint32_t sh = 8 * (j & 3);
-        const int q = j >> 2;
-        ins[0] |= (q == 0) ? v << sh : 0u;
-        ins[1] |= (q == 1) ? v << sh : 0u;
-        ins[2] |= (q == 2) ? v << sh : 0u;
-        ins[3] |= (q == 3) ? v << sh : 0u;
       }
-      E[0] |= ins[0]; E[1] |= ins[1]; E[2] |= ins[2]; E[3] |= ins[3];
+      const uint4 d = *reinterpret_cast<const uint4*>(slot);
+      E0 |= d.x; E1 |= d.y; E2 |= d.z; E3 |= d.w;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
 
     // ---- reassemble (codec.py:308-312) and store ---------------------------
-    if (write_out && nvalid > 0) {
-      uint32_t o[8];
-      reassemble4(sv.x, E[0], o[0], o[1]);
-      reassemble4(sv.y, E[1], o[2], o[3]);
-      reassemble4(sv.z, E[2], o[4], o[5]);
-      reassemble4(sv.w, E[3], o[6], o[7]);
+    if (write_out && nv > 0) {
+      uint32_t o0, o1, o2, o3, o4, o5, o6, o7;
+      reassemble4(sv.x, E0, o0, o1);
+      reassemble4(sv.y, E1, o2, o3);
+      reassemble4(sv.z, E2, o4, o5);
+      reassemble4(sv.w, E3, o6, o7);
       uint16_t* dst = out + segs.out_off[seg] + base;
-      if (full_t && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-        st_stream_v4(dst, make_uint4(o[0], o[1], o[2], o[3]));
-        st_stream_v4(dst + 8, make_uint4(o[4], o[5], o[6], o[7]));
+      if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
+        st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
       } else {
-        const int lim = full_t ? kEPT : (int)nvalid;
-        for (int j = 0; j < lim; ++j) dst[j] = (uint16_t)(o[j >> 1] >> (16 * (j & 1)));
+        const uint32_t ow[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
+#pragma unroll
+        for (int j = 0; j < kEPT; ++j)
+          if (j < nv) dst[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
       }
     }
   }

@@ -427,8 +427,9 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       *reinterpret_cast<uint16_t*>(frame + L.off[2] + pb) = (uint16_t)p1;
       *reinterpret_cast<uint16_t*>(frame + L.off[3] + pb) = (uint16_t)p2;
     } else if (nvalid > 0) {
-      for (int j = 0; j < nvalid; ++j)
-        frame[L.off[0] + base + j] = (uint8_t)(sm[j >> 2] >> (8 * (j & 3)));
+#pragma unroll
+      for (int j = 0; j < kEPT; ++j)
+        if (j < nvalid) frame[L.off[0] + base + j] = (uint8_t)(sm[j >> 2] >> (8 * (j & 3)));
       const int64_t pb = base >> 3;
       frame[L.off[1] + pb] = (uint8_t)p0;
       frame[L.off[2] + pb] = (uint8_t)p1;
@@ -446,17 +447,18 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+      incl += (lane >= o) ? v : 0u;
     }
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();                                      // (B)
-    uint32_t wbase = 0, agg = 0;
+    uint32_t wv = lane < kWarps ? s_warp[lane] : 0u, wi = wv;
 #pragma unroll
-    for (int i = 0; i < kWarps; ++i) {
-      const uint32_t v = s_warp[i];
-      wbase += (i < warp) ? v : 0u;
-      agg += v;
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      wi += (lane >= o) ? u : 0u;
     }
+    const uint32_t wbase = __shfl_sync(0xffffffffu, wi - wv, warp);
+    const uint32_t agg = __shfl_sync(0xffffffffu, wi, kWarps - 1);
     const uint32_t lp = run + wbase + incl - cnt;   // run-relative escape prefix
 
     // ---- run-relative group index -------------------------------------------
