@@ -486,7 +486,9 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
   // scan.  Mode B (1024 <= gs <= 4096): groups span warps; block scan.
   const int ct = tid - 32, lane = ct & 31, warp = ct >> 5;
   const bool modeA = gsl <= 9;
+  const bool gs512 = gsl == 9;
   uint8_t* slot = s_slot + ct * kEPT;
+  uint16_t* const out_seg = out + segs.out_off[seg];
   int32_t my_err = kOk;
   for (int64_t t = t_begin; t < t_end; ++t) {
     const int64_t k = t - t_begin;
@@ -495,7 +497,10 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     const DStage& S = ring[st];
     const int64_t tile_base = t * kTile;
     const int64_t base = tile_base + (int64_t)ct * kEPT;
-    const int nv = (int)((n - base) < kEPT ? (n - base) : kEPT);   // may be <= 0
+    const int64_t rem = n - tile_base;                       // >= 1
+    const int rem32 = rem >= kTile ? kTile : (int)rem;
+    const int nv = rem32 - ct * kEPT >= kEPT ? kEPT : rem32 - ct * kEPT;   // may be <= 0
+    const int live_warps = (rem32 + 511) >> 9;
     const uint32_t valid16 = nv >= kEPT ? 0xFFFFu : (nv > 0 ? ((1u << nv) - 1u) : 0u);
     const int64_t lo = s_lo[st];
     const int32_t tcnt = (int32_t)s_cnt[st];
@@ -526,7 +531,19 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     }
     const uint32_t wexcl = incl - cnt;               // escapes in the warp before me
     int32_t rank0;                                   // tile-local rank of my first escape
-    if (modeA) {
+    if (gs512) {
+      // fast path (collectives): one group per warp, 32-bit math, staged slice
+      const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+      const bool warp_live = warp < live_warps;
+      const uint32_t gwv = warp_live ? S.gi[gshift + warp] : 0u;
+      rank0 = (int32_t)(gwv - (uint32_t)lo + wexcl);
+      if (lane == 0 && warp_live) {
+        const int64_t g = g0 + warp;
+        const uint32_t next = (g + 1 < L.groups) ? S.gi[gshift + warp + 1] : (uint32_t)H.zc;
+        if (g == 0 && gwv != 0) my_err = kErrGroupIndex;
+        if (gwv + wtot != next) my_err = (g + 1 < L.groups) ? kErrGroupIndex : kErrZeroCount;
+      }
+    } else if (modeA) {
       const int64_t gw = (tile_base + warp * 512) >> gsl;     // warp's first group
       const bool warp_live = tile_base + warp * 512 < n;
       const int32_t wbase = warp_live ? (int32_t)(gi_at(gw) - lo) : 0;
@@ -592,21 +609,22 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     }
     // ---- escapes: staged bytes at their tile-local rank -> per-thread slot ---
     if (esc) {
-      *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
-      const uint8_t* eb = S.esc + esc_off;
-      uint32_t m = esc;
-      int32_t r = rank0;
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        uint8_t v = 0;
-        if ((uint32_t)r < (uint32_t)tcnt) v = eb[r];
-        else my_err = kErrZeroCount;   // always accompanied by a failing index check
-        slot[j] = v;
-        ++r;
+      if (rank0 < 0 || rank0 + (int32_t)cnt > tcnt) {
+        // escapes out of the staged range: always accompanied by a failing
+        // index check, which carries the field the reference names
+        my_err = kErrZeroCount;
+      } else {
+        *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
+        const uint8_t* eb = S.esc + esc_off + rank0;
+        uint32_t m = esc;
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          slot[j] = *eb++;
+        }
+        const uint4 d = *reinterpret_cast<const uint4*>(slot);
+        E0 |= d.x; E1 |= d.y; E2 |= d.z; E3 |= d.w;
       }
-      const uint4 d = *reinterpret_cast<const uint4*>(slot);
-      E0 |= d.x; E1 |= d.y; E2 |= d.z; E3 |= d.w;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
@@ -618,7 +636,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
       reassemble4(sv.y, E1, o2, o3);
       reassemble4(sv.z, E2, o4, o5);
       reassemble4(sv.w, E3, o6, o7);
-      uint16_t* dst = out + segs.out_off[seg] + base;
+      uint16_t* dst = out_seg + base;
       if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
         st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
         st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
