@@ -1,0 +1,291 @@
+"""Communicator seam — replaces reference transport.py (Communicator,
+exchange_sizes, TrafficStats, run_ranks; transport.py:46-88, :559-671).
+
+The reference moves bytes with Python sockets and queues.  Here the host
+side agrees on sizes and the device side moves frames:
+
+* ``DistCommunicator`` wraps a ``torch.distributed`` process group.  With the
+  NCCL backend the byte movers are NCCL collectives / grouped send-recv over
+  NVLink on device tensors; with gloo (CPU tests, or several ranks sharing
+  one GPU) they stage through host memory.
+* ``HubCommunicator`` binds in-process thread ranks (``run_ranks``), the
+  analogue of the reference's loopback hub: frames move with device copies.
+
+Every communicator keeps the reference's ``TrafficStats`` byte counters.
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass
+
+import torch
+
+from .errors import ProtocolError, TransportError
+
+DEFAULT_TIMEOUT = 30.0
+
+
+@dataclass
+class TrafficStats:
+    """Bytes this rank put on the wire (reference transport.py:559-573)."""
+
+    bytes_sent: int = 0
+    bytes_received: int = 0
+    messages_sent: int = 0
+
+    def snapshot(self) -> "TrafficStats":
+        return TrafficStats(self.bytes_sent, self.bytes_received, self.messages_sent)
+
+    def delta(self, earlier: "TrafficStats") -> "TrafficStats":
+        return TrafficStats(self.bytes_sent - earlier.bytes_sent,
+                            self.bytes_received - earlier.bytes_received,
+                            self.messages_sent - earlier.messages_sent)
+
+
+class Communicator:
+    """A rank bound into a group of ``world_size`` peers (transport.py:576-623)."""
+
+    rank: int
+    world_size: int
+    device: torch.device
+
+    def __init__(self):
+        self.stats = TrafficStats()
+
+    # -- reference surface -------------------------------------------------------
+    def peers(self) -> list:
+        return [r for r in range(self.world_size) if r != self.rank]
+
+    def now(self) -> float:
+        return time.perf_counter()
+
+    def exchange_sizes(self, local_sizes, tag: int = 0) -> list:
+        """All-to-all of one u64 per peer; entry p is what peer p declared for
+        this rank, the self entry passes through (transport.py:607-623)."""
+        sizes = [int(s) for s in local_sizes]
+        if len(sizes) != self.world_size:
+            raise ValueError(f"expected {self.world_size} sizes, got {len(sizes)}")
+        got = self._a2a_ints(sizes)
+        got[self.rank] = sizes[self.rank]
+        self._count(8 * (self.world_size - 1), self.world_size - 1)
+        return got
+
+    def allgather_ints(self, value: int) -> list:
+        return self._allgather_ints(int(value))
+
+    # -- byte movers (device tensors) ------------------------------------------
+    def all_gather_bytes(self, send: torch.Tensor, recv: torch.Tensor) -> None:
+        """recv[p*len(send):(p+1)*len(send)] = send of rank p (equal sizes)."""
+        raise NotImplementedError
+
+    def sendrecv_bytes(self, sends: dict, recvs: dict) -> None:
+        """Grouped point-to-point: sends {peer: tensor}, recvs {peer: tensor}."""
+        raise NotImplementedError
+
+    def barrier(self) -> None:
+        raise NotImplementedError
+
+    # -- helpers -----------------------------------------------------------------
+    def _count(self, nbytes: int, nmsg: int = 1) -> None:
+        self.stats.bytes_sent += int(nbytes)
+        self.stats.messages_sent += int(nmsg)
+
+    @classmethod
+    def from_process_group(cls, group=None, device=None) -> "DistCommunicator":
+        return DistCommunicator(group, device)
+
+
+class DistCommunicator(Communicator):
+    """Over a torch.distributed group: NCCL moves device bytes over NVLink."""
+
+    def __init__(self, group=None, device=None):
+        super().__init__()
+        import torch.distributed as dist
+        self._dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world_size = dist.get_world_size(group)
+        self.backend = dist.get_backend(group)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) \
+                if torch.cuda.is_available() else torch.device("cpu")
+        self.device = torch.device(device)
+        self.on_device = self.backend == "nccl"
+
+    def _wire(self, t: torch.Tensor) -> torch.Tensor:
+        return t if self.on_device else t.cpu()
+
+    def _allgather_ints(self, value: int) -> list:
+        dev = self.device if self.on_device else torch.device("cpu")
+        src = torch.tensor([value], dtype=torch.int64, device=dev)
+        out = torch.empty(self.world_size, dtype=torch.int64, device=dev)
+        self._dist.all_gather_into_tensor(out, src, group=self.group)
+        return [int(v) for v in out.cpu().tolist()]
+
+    def _a2a_ints(self, sizes: list) -> list:
+        dev = self.device if self.on_device else torch.device("cpu")
+        src = torch.tensor(sizes, dtype=torch.int64, device=dev)
+        out = torch.empty(self.world_size, dtype=torch.int64, device=dev)
+        self._dist.all_to_all_single(out, src, group=self.group)
+        return [int(v) for v in out.cpu().tolist()]
+
+    def all_gather_bytes(self, send: torch.Tensor, recv: torch.Tensor) -> None:
+        if self.on_device:
+            self._dist.all_gather_into_tensor(recv, send, group=self.group)
+        else:
+            r = torch.empty(recv.numel(), dtype=recv.dtype)
+            self._dist.all_gather_into_tensor(r, send.cpu(), group=self.group)
+            recv.copy_(r)
+        self._count(send.numel() * send.element_size() * (self.world_size - 1),
+                    self.world_size - 1)
+
+    def sendrecv_bytes(self, sends: dict, recvs: dict) -> None:
+        dist = self._dist
+        staged = {}
+        ops = []
+        for p, t in sends.items():
+            if t.numel():
+                ops.append(dist.P2POp(dist.isend, self._wire(t.contiguous()), p, self.group))
+                self._count(t.numel() * t.element_size())
+        for p, t in recvs.items():
+            if t.numel():
+                buf = t if self.on_device else torch.empty(t.numel(), dtype=t.dtype)
+                staged[p] = buf
+                ops.append(dist.P2POp(dist.irecv, buf, p, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        if not self.on_device:
+            for p, buf in staged.items():
+                recvs[p].copy_(buf)
+
+    def barrier(self) -> None:
+        self._dist.barrier(group=self.group)
+
+
+class _Hub:
+    """Shared state of in-process thread ranks (reference _LoopbackHub,
+    transport.py:46-88).  Exchanges are keyed by a per-rank generation
+    counter, so an abort only reaches ranks that are still waiting."""
+
+    def __init__(self, world_size: int):
+        self.world_size = world_size
+        self.cond = threading.Condition()
+        self.gen = [0] * world_size
+        self.slots: dict = {}
+        self.error: BaseException | None = None
+
+    def exchange(self, rank: int, obj) -> list:
+        with self.cond:
+            g = self.gen[rank]
+            self.gen[rank] += 1
+            self.slots.setdefault(g, {})[rank] = obj
+            self.cond.notify_all()
+            while len(self.slots[g]) < self.world_size:
+                if self.error is not None:
+                    raise TransportError(f"communicator aborted: {self.error}")
+                if not self.cond.wait(timeout=DEFAULT_TIMEOUT):
+                    from .errors import TransportTimeout
+                    raise TransportTimeout(f"rank {rank} timed out in exchange {g}")
+            vals = [self.slots[g][r] for r in range(self.world_size)]
+            # every rank that posted g has finished reading g - 1
+            self.slots.pop(g - 1, None)
+            return vals
+
+    def abort(self, exc: BaseException) -> None:
+        with self.cond:
+            if self.error is None:
+                self.error = exc
+            self.cond.notify_all()
+
+    def sync(self, rank: int) -> None:
+        self.exchange(rank, None)
+
+
+class HubCommunicator(Communicator):
+    """Thread rank on a shared hub; each rank has its own CUDA stream."""
+
+    def __init__(self, hub: _Hub, rank: int, device):
+        super().__init__()
+        self.hub = hub
+        self.rank = rank
+        self.world_size = hub.world_size
+        self.device = torch.device(device)
+        self.stream = torch.cuda.Stream(device=self.device)
+
+    def _post_and_collect(self, obj) -> list:
+        return self.hub.exchange(self.rank, obj)
+
+    def _allgather_ints(self, value: int) -> list:
+        return [int(v) for v in self._post_and_collect(int(value))]
+
+    def _a2a_ints(self, sizes: list) -> list:
+        rows = self._post_and_collect(list(sizes))
+        return [int(rows[p][self.rank]) for p in range(self.world_size)]
+
+    def all_gather_bytes(self, send: torch.Tensor, recv: torch.Tensor) -> None:
+        torch.cuda.current_stream(self.device).synchronize()
+        srcs = self._post_and_collect(send)
+        n = send.numel()
+        for p, src in enumerate(srcs):
+            if src.numel() != n:
+                raise ProtocolError(f"all-gather size mismatch with rank {p}")
+            recv[p * n:(p + 1) * n].copy_(src)
+        torch.cuda.current_stream(self.device).synchronize()
+        self.hub.sync(self.rank)
+        self._count(n * send.element_size() * (self.world_size - 1), self.world_size - 1)
+
+    def sendrecv_bytes(self, sends: dict, recvs: dict) -> None:
+        torch.cuda.current_stream(self.device).synchronize()
+        posted = self._post_and_collect({p: t for p, t in sends.items()})
+        for p, t in recvs.items():
+            if t.numel():
+                src = posted[p].get(self.rank)
+                if src is None or src.numel() != t.numel():
+                    got = 0 if src is None else src.numel()
+                    raise ProtocolError(f"rank {p} sent {got} bytes, expected {t.numel()}")
+                t.copy_(src)
+        torch.cuda.current_stream(self.device).synchronize()
+        self.hub.sync(self.rank)
+        for t in sends.values():
+            if t.numel():
+                self._count(t.numel() * t.element_size())
+
+    def barrier(self) -> None:
+        torch.cuda.current_stream(self.device).synchronize()
+        self.hub.sync(self.rank)
+
+
+def run_ranks(world_size: int, fn, device=None, timeout: float = DEFAULT_TIMEOUT) -> list:
+    """Run fn(comm) on ``world_size`` in-process thread ranks sharing one GPU
+    (or ``device`` per rank when a list is given); results by rank
+    (reference run_ranks, transport.py:635-666).  The first failure aborts
+    the hub so peers error out instead of hanging, and is re-raised."""
+    hub = _Hub(world_size)
+    results = [None] * world_size
+    failures = []
+    devs = device if isinstance(device, (list, tuple)) else [device] * world_size
+
+    def body(rank: int) -> None:
+        dev = devs[rank] if devs[rank] is not None else torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        comm = HubCommunicator(hub, rank, dev)
+        try:
+            with torch.cuda.stream(comm.stream):
+                results[rank] = fn(comm)
+                torch.cuda.current_stream().synchronize()
+        except BaseException as exc:  # noqa: BLE001 - propagated to the caller
+            failures.append((rank, exc))
+            hub.abort(exc)
+
+    threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world_size)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=timeout * 10)
+    if failures:
+        rank, exc = min(failures, key=lambda f: f[0])
+        raise exc
+    return results

@@ -1,0 +1,93 @@
+"""Host logic on CPU: the switcher's decision rule / fit (reference
+tests/test_switcher.py:25-104, acceptance criterion 7 closed forms) and the
+communicator seam over a 2-rank gloo group (reference
+tests/test_transport.py:105-113 transpose oracle)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2604_27844_b200.switcher import (CostModel, Path, crossover, fit_cost_model, predict,
+                                            scaled, select)
+
+
+def test_predict_select_crossover():
+    m = CostModel(alpha_rs=1e-5, beta_rs=2e-9, alpha_a2a=6e-5, beta_a2a=1.8e-9, e=0.7)
+    d_star = crossover(m)
+    assert d_star == pytest.approx((6e-5 - 1e-5) / (2e-9 - 1.8e-9 * 0.7))
+    scan = [d for d in range(0, int(d_star * 2), 997) if select(m, d) is Path.ZIPPED]
+    assert scan and min(scan) == pytest.approx(d_star, abs=997)
+    for d in range(0, int(d_star * 2), 997):
+        assert select(m, d) is select(scaled(m, 13.7), d)
+    t_rs, t_a2a = predict(m, 0)
+    assert select(m, 0) is Path.NATIVE and t_rs < t_a2a
+
+
+def test_tie_goes_native():
+    m = CostModel(1e-5, 1e-9, 1e-5, 1e-9, e=1.0)
+    assert select(m, 12345) is Path.NATIVE
+    assert crossover(m) is None
+
+
+def test_exact_two_point_fit():
+    sizes = [1 << 16, 1 << 24]
+    t_rs = [2e-5 + 3e-10 * d for d in sizes]
+    t_zip = [5e-5 + 4e-10 * 0.7 * d for d in sizes]
+    m = fit_cost_model(sizes, t_rs, t_zip, e=0.7)
+    assert m.alpha_rs == pytest.approx(2e-5) and m.beta_rs == pytest.approx(3e-10)
+    assert m.alpha_a2a == pytest.approx(5e-5) and m.beta_a2a == pytest.approx(4e-10)
+
+
+def test_validation_and_file_round_trip(tmp_path):
+    with pytest.raises(ValueError):
+        CostModel(-1, 0, 0, 0, 0.5)
+    with pytest.raises(ValueError):
+        CostModel(0, 0, 0, 0, 1.5)
+    with pytest.raises(ValueError):
+        fit_cost_model([1, 1], [1, 2], [1, 2], e=0.5)
+    m = CostModel(1e-5, 2e-9, 6e-5, 1.8e-9, 0.7)
+    m.to_file(tmp_path / "p.txt")
+    assert CostModel.from_file(tmp_path / "p.txt") == m
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _seam_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2604_27844_b200.transport import Communicator
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = Communicator.from_process_group(device="cpu")
+    sizes = [100 * rank + p for p in range(world)]
+    got = comm.exchange_sizes(sizes)
+    gathered = comm.allgather_ints(7 + rank)
+    comm.barrier()
+    q.put((rank, got, gathered, comm.stats.bytes_sent))
+    dist.destroy_process_group()
+
+
+def test_exchange_sizes_transpose_over_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seam_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (g, a, b)) for r, g, a, b in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        got, gathered, sent = res[r]
+        # entry p = what peer p declared for this rank; self passes through
+        assert got == [100 * p + r if p != r else 100 * r + r for p in range(world)]
+        assert gathered == [7, 8]
+        assert sent == 8 * (world - 1)
