@@ -125,6 +125,20 @@ class ClockSampler:
                            "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _agreed_steps(seconds, step, world, dev):
+    """Number of untimed steps filling ~`seconds`, identical on every rank."""
+    import torch
+    t = time.perf_counter()
+    step()
+    torch.cuda.synchronize()
+    per = max(time.perf_counter() - t, 1e-4)
+    k = torch.tensor([max(1, int(seconds / per))], device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(k, op=dist.ReduceOp.MAX)
+    return int(k.item())
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -205,10 +219,15 @@ def run_ours(args):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    if args.share_gpu:
+        local = 0          # test mode: all ranks on one GPU, gloo moves the bytes
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
     from paper_2604_27844_b200 import engine
     if world > 1:
         from paper_2604_27844_b200 import collectives as coll
@@ -247,8 +266,8 @@ def run_ours(args):
         comm = coll.Communicator.from_process_group()
 
         def step(rec=False):
-            return coll.zip_all_gather(comm, shard, _return_device=True)
-        launches_per_step = None
+            return coll.zip_all_gather(comm, shard)
+        launches_per_step = 5          # stats, finalize, encode pass 1 + fix-up, batched decode
 
     # correctness gate before timing: bit-exact round trip
     err = step()
@@ -269,20 +288,21 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         # keep the GPU under the same load while nvidia-smi starts sampling,
         # so the clocks reflect the timed steps (the timed region itself is ms)
-        tb = time.perf_counter()
-        while time.perf_counter() - tb < args.clock_settle:
+        settle = _agreed_steps(args.clock_settle, step, world, dev)
+        for _ in range(settle):
             step()
-            torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0.record(stream)
         for _ in range(args.steps):
             step(rec=(world == 1))
         t1.record(stream)
         torch.cuda.synchronize()
-        tb = time.perf_counter()
-        while time.perf_counter() - tb < 0.3:
+        for _ in range(max(1, settle // 3)):
             step()
-            torch.cuda.synchronize()
+        torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -290,6 +310,25 @@ def run_ours(args):
         ms = float(tt.item())
     total_bytes = world * 2 * LAYER_ELEMS          # gathered output bytes, all ranks
     value = total_bytes / (ms / 1e3) / 1e9
+    raw = None
+    if world > 1:
+        # the plain uncompressed collective on the same shards, same run
+        for _ in range(args.warmup):
+            coll.reference_all_gather(comm, shard)
+        torch.cuda.synchronize()
+        dist.barrier()
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(args.steps):
+            coll.reference_all_gather(comm, shard)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        rt = torch.tensor([r0.elapsed_time(r1) / args.steps], device=dev)
+        dist.all_reduce(rt, op=dist.ReduceOp.MAX)
+        raw_ms = float(rt.item())
+        raw = {"value": total_bytes / (raw_ms / 1e3) / 1e9, "ms_per_step": raw_ms,
+               "backend": args.backend, "speedup_zip_over_raw": raw_ms / ms}
 
     # ---- roofline of the dominant kernel (decode) ---------------------------
     roof = None
@@ -355,7 +394,8 @@ def run_ours(args):
                            "parallelism": f"dp{world}", "group_size": 512,
                            "frame_bytes": frame_bytes,
                            "ratio": (2 * n / frame_bytes) if frame_bytes else None,
-                           "l2": "inputs (436 MB) larger than L2 (126 MB); no flush"},
+                           "l2": "inputs (436 MB) larger than L2 (126 MB); no flush",
+                           "uncompressed_collective": raw},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
                 "clocks": clk.result}
@@ -373,6 +413,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-settle", type=float, default=1.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test mode: every rank on cuda:0 (use with --backend gloo)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
