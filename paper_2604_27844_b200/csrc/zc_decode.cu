@@ -490,7 +490,86 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
   uint8_t* slot = s_slot + ct * kEPT;
   uint16_t* const out_seg = out + segs.out_off[seg];
   int32_t my_err = kOk;
-  for (int64_t t = t_begin; t < t_end; ++t) {
+  // tiles [t_begin, t_fast_end) are full and take the lean gs = 512 path
+  const int64_t t_fast_end = gs512 ? (n / kTile < t_end ? n / kTile : t_end) : t_begin;
+  const bool out_aligned = ((reinterpret_cast<uintptr_t>(out_seg) & 15) == 0) && write_out;
+  const int ntl = (int)(t_end - t_begin);
+  const int nfast = (int)(t_fast_end > t_begin ? t_fast_end - t_begin : 0);
+  const uint32_t zc32 = (uint32_t)H.zc;
+  const uint32_t ngroups32 = (uint32_t)L.groups;
+  const uint32_t g_begin = (uint32_t)(t_begin * gpt);
+  for (int k = 0; k < nfast; ++k) {
+    // ---------------- lean path: gs = 512, all 16 elements valid -----------
+    const int st = k & (kDStages - 1);
+    mbar_wait(full + st, (uint32_t)((k / kDStages) & 1));
+    const DStage& S = ring[st];
+    const uint4 sv = *reinterpret_cast<const uint4*>(S.sm + ct * kEPT);
+    const uint32_t p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + ct * 2);
+    const uint32_t p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + ct * 2);
+    const uint32_t p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
+    const uint32_t esc = ~(p0 | p1 | p2) & 0xFFFFu;
+    const uint32_t cnt = __popc(esc);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      incl += (lane >= o) ? v : 0u;
+    }
+    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+    const int gshift = s_gi_shift[st];
+    const uint32_t lo32 = (uint32_t)s_lo[st];
+    const int32_t tcnt = (int32_t)s_cnt[st];
+    const int32_t esc_off = (int32_t)(s_lo[st] - s_al[st]);
+    const uint32_t gwv = S.gi[gshift + warp];
+    const int32_t rank0 = (int32_t)(gwv - lo32 + incl - cnt);
+    if (lane == 0) {
+      const uint32_t g = g_begin + (uint32_t)k * 8u + (uint32_t)warp;
+      const bool has_next = g + 1 < ngroups32;
+      const uint32_t next = has_next ? S.gi[gshift + warp + 1] : zc32;
+      if (g == 0 && gwv != 0) my_err = kErrGroupIndex;
+      if (gwv + wtot != next) my_err = has_next ? kErrGroupIndex : kErrZeroCount;
+    }
+    const uint32_t lo8 = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
+    const uint32_t hi8 = s_spread[p0 >> 8] | s_spread[p1 >> 8] << 1 | s_spread[p2 >> 8] << 2;
+    uint32_t E0 = prmt(H.tbl_lo, H.tbl_hi, lo8);
+    uint32_t E1 = prmt(H.tbl_lo, H.tbl_hi, lo8 >> 16);
+    uint32_t E2 = prmt(H.tbl_lo, H.tbl_hi, hi8);
+    uint32_t E3 = prmt(H.tbl_lo, H.tbl_hi, hi8 >> 16);
+    if (esc) {
+      if (rank0 < 0 || rank0 + (int32_t)cnt > tcnt) {
+        my_err = kErrZeroCount;     // accompanied by a failing index check
+      } else {
+        *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
+        const uint8_t* eb = S.esc + esc_off + rank0;
+        uint32_t m = esc;
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          slot[j] = *eb++;
+        }
+        const uint4 d = *reinterpret_cast<const uint4*>(slot);
+        E0 |= d.x; E1 |= d.y; E2 |= d.z; E3 |= d.w;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+    uint32_t o0, o1, o2, o3, o4, o5, o6, o7;
+    reassemble4(sv.x, E0, o0, o1);
+    reassemble4(sv.y, E1, o2, o3);
+    reassemble4(sv.z, E2, o4, o5);
+    reassemble4(sv.w, E3, o6, o7);
+    uint16_t* dst = out_seg + ((t_begin + k) * kTile + ct * kEPT);
+    if (out_aligned) {
+      st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
+      st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
+    } else if (write_out) {
+      const uint32_t ow[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
+#pragma unroll
+      for (int j = 0; j < kEPT; ++j) dst[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
+    }
+  }
+  for (int64_t t = t_begin + nfast; t < t_end; ++t) {
+    // ---------------- general path ---------------------------------------
     const int64_t k = t - t_begin;
     const int st = (int)(k % kDStages);
     mbar_wait(full + st, (uint32_t)((k / kDStages) & 1));
