@@ -358,7 +358,100 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
   __syncthreads();
 
   uint32_t run = 0;   // escapes of this run before the current tile
-  for (int64_t t = t_begin; t < t_end; ++t) {
+  // ---- lean loop: aligned input, tile fully inside the segment ---------------
+  const int64_t t_full_end = aligned ? ((n / kTile) < t_end ? (n / kTile) : t_end) : t_begin;
+  const int nfast = (int)(t_full_end > t_begin ? t_full_end - t_begin : 0);
+  {
+    uint8_t* p_sm = frame + L.off[0] + t_begin * kTile + tid * kEPT;
+    uint8_t* p_pl0 = frame + L.off[1] + (t_begin * kTile + tid * kEPT) / 8;
+    const int64_t pl_stride = L.off[2] - L.off[1];
+    uint32_t* gi_w = gi + ((t_begin * kTile + tid * kEPT) >> 9);
+    const bool gi512 = gsl == 9;
+    for (int k = 0; k < nfast; ++k) {
+      const int st = k & (kStages - 1);
+      const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
+      mbar_wait(bars + st, (uint32_t)((k / kStages) & 1));
+      const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
+      const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t sm[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t p = prmt(w[2 * j], w[2 * j + 1], 0x6420);
+        const uint32_t q = prmt(w[2 * j], w[2 * j + 1], 0x7531);
+        sm[j] = (p & 0x7F7F7F7Fu) | (q & 0x80808080u);
+      }
+      uint32_t A = 0, B = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t wl = w[j >> 1];
+        const uint32_t off = (j & 1) ? __umulhi(wl & 0x7F800000u, 1u << 11)
+                                     : __umulhi(wl & 0x00007F80u, 1u << 27);
+        A += *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(s_lut) + off) << j;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t wl = w[4 + (j >> 1)];
+        const uint32_t off = (j & 1) ? __umulhi(wl & 0x7F800000u, 1u << 11)
+                                     : __umulhi(wl & 0x00007F80u, 1u << 27);
+        B += *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(s_lut) + off) << j;
+      }
+      st_stream_v4(p_sm, make_uint4(sm[0], sm[1], sm[2], sm[3]));
+      *reinterpret_cast<uint16_t*>(p_pl0) = (uint16_t)prmt(A, B, 0x40);
+      *reinterpret_cast<uint16_t*>(p_pl0 + pl_stride) = (uint16_t)prmt(A, B, 0x51);
+      *reinterpret_cast<uint16_t*>(p_pl0 + 2 * pl_stride) = (uint16_t)prmt(A, B, 0x62);
+      const uint32_t esc = prmt(A, B, 0x73) & 0xFFFFu;
+      const uint32_t cnt = __popc(esc);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        incl += (lane >= o) ? v : 0u;
+      }
+      if (lane == 31) s_warp[warp] = incl;
+      __syncthreads();                                    // (B)
+      const uint32_t wv = lane < kWarps ? s_warp[lane] : 0u;
+      uint32_t wi = wv;
+#pragma unroll
+      for (int o = 1; o < kWarps; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+        wi += (lane >= o) ? u : 0u;
+      }
+      const uint32_t wbase = __shfl_sync(0xffffffffu, wi - wv, warp);
+      const uint32_t agg = __shfl_sync(0xffffffffu, wi, kWarps - 1);
+      const uint32_t lp = run + wbase + incl - cnt;
+      if (gi512) {
+        if (lane == 0) *gi_w = lp;
+      } else if (gsl >= 4) {
+        const int64_t base = (t_begin + k) * kTile + (int64_t)tid * kEPT;
+        if ((base & ((int64_t(1) << gsl) - 1)) == 0) gi[base >> gsl] = lp;
+      } else {
+        const int64_t base = (t_begin + k) * kTile + (int64_t)tid * kEPT;
+        const int gs = 1 << gsl;
+        for (int j = 0; j < kEPT; j += gs)
+          gi[(base + j) >> gsl] = lp + __popc(esc & ((1u << j) - 1u));
+      }
+      if (esc) {
+        uint8_t* dst = esc_out + lp;
+        uint32_t m = esc;
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          *dst++ = (uint8_t)((tw[tid * kEPT + j] >> 7) & 0xFFu);
+        }
+      }
+      run += agg;
+      __syncthreads();                                    // (C) stage + s_warp free
+      if (tid == 0 && t_begin + k + kStages < t_end) {
+        fence_proxy_async();
+        encode_issue(xs, n, t_begin + k + kStages, ring + st * kStageBytes, bars + st);
+      }
+      p_sm += kTile;
+      p_pl0 += kTile / 8;
+      gi_w += kTile / 512;
+    }
+  }
+  for (int64_t t = t_begin + nfast; t < t_end; ++t) {
     const int64_t k = t - t_begin;
     const int st = (int)(k % kStages);
     const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
