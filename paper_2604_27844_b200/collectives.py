@@ -156,6 +156,8 @@ def zip_all_gather(comm: Communicator, local, sigma: float | None = None,
                    _return_device: bool = True) -> torch.Tensor:
     """All-gather with compressed payloads, bit-identical to the reference
     all-gather (collectives.py:203-227)."""
+    if getattr(comm, "use_p2p", False):
+        return zip_all_gather_p2p(comm, local, sigma)
     dev = _dev(comm)
     words = device_words(local, dev)
     n = words.numel()
@@ -366,3 +368,55 @@ def timed_call(comm: Communicator, fn):
         torch.cuda.current_stream().synchronize()
     elapsed = comm.now() - start
     return result, max(allgather_scalar(comm, elapsed))
+
+
+# ---------------------------------------------------------------------------
+# peer-memory (NVLink) pull-decode variants — SURVEY K5 "fused pull-decode"
+
+def _use_p2p(comm: Communicator) -> bool:
+    return bool(getattr(comm, "use_p2p", isinstance(comm, HubCommunicator)))
+
+
+def zip_all_gather_p2p(comm: Communicator, local, sigma: float | None = None) -> torch.Tensor:
+    """All-gather where the transfer IS the decode: every rank encodes its
+    shard into its own symmetric buffer, signals its peers device-side, and
+    each rank's decoder pulls the peer frames over NVLink (TMA from peer HBM)
+    straight into the gathered output.  Bit-identical to reference_all_gather."""
+    from .peer import workspace_for
+    dev = _dev(comm)
+    words = device_words(local, dev)
+    n = words.numel()
+    W = comm.world_size
+    if W == 1:
+        return words.clone()
+    counts = comm.allgather_ints(n)
+    if n == 0:
+        for p, c in enumerate(counts):
+            if c != 0:
+                raise ProtocolError(f"all-gather frame size mismatch: rank {comm.rank} has 0, "
+                                    f"rank {p} declared {c}")
+        return torch.empty(0, dtype=torch.int16, device=dev)
+    for p, c in enumerate(counts):
+        if c != n:
+            raise CollectiveError(f"frame holds {c} elements, expected {n}", peer=p)
+    ws = workspace_for(comm, engine.max_frame_bytes(max(counts), GS_LOG2))
+    e = ws.epoch + 1
+    ws.epoch = e
+    werr = torch.full((1,), engine.ERR_OK, dtype=torch.int32, device=dev)
+    if e > 1:
+        ws.wait(1, e - 1, werr)                 # peers finished reading my last frame
+    book = codec.device_codebook(words, sigma)
+    flen = engine.encode(words, [(0, n)], book, GS_LOG2, ws.buf, [256])
+    ws.signal(0, e)                             # my frame is ready
+    ws.wait(0, e, werr)                         # every peer's frame is ready
+    out = torch.empty(W * n, dtype=torch.int16, device=dev)
+    peers = comm.peers()
+    err = engine.decode([ws.peer_base[p] + 256 for p in peers], [0] * len(peers), None,
+                        [n] * len(peers), out, [p * n for p in peers])
+    ws.signal(1, e)                             # done reading the peers' frames
+    out[comm.rank * n:(comm.rank + 1) * n].copy_(words)
+    del flen
+    if int(werr.item()) != engine.ERR_OK:
+        raise CollectiveError("peer frame never became ready (timeout)")
+    _raise_decode_errors(err, peers)
+    return out

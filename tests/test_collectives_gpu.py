@@ -222,3 +222,18 @@ def test_fuzz_against_reference():
                         return False
                 return True
             assert all(run_ranks(world, body)), (world, seed)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_all_gather_p2p_pull_decode(world):
+    from paper_2604_27844_b200.collectives import zip_all_gather_p2p
+
+    def body(comm):
+        outs = []
+        for it in range(3):   # epochs: buffer reuse is guarded by the done flags
+            local = rank_words(comm.rank + 10 * it, 300_007, sigma=0.02)
+            outs.append((H(zip_all_gather_p2p(comm, local)), H(reference_all_gather(comm, local))))
+        return outs
+    for outs in run_ranks(world, body):
+        for z, r in outs:
+            assert np.array_equal(z, r)

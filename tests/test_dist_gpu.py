@@ -55,6 +55,50 @@ def _worker(rank, world, port, q):
         q.put((rank, False, traceback.format_exc()))
 
 
+def _p2p_worker(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2604_27844_b200.collectives import reference_all_gather, zip_all_gather
+        from paper_2604_27844_b200.transport import Communicator
+        from tests.conftest import rank_words
+        comm = Communicator.from_process_group(device="cuda:0")
+        comm.use_p2p = True           # CUDA IPC symmetric buffers, device-side signals
+        H = lambda t: t.cpu().numpy().view(np.uint16)  # noqa: E731
+        ok = True
+        for it in range(3):
+            local = rank_words(rank + 7 * it, 500_009, sigma=0.02)
+            ok &= np.array_equal(H(zip_all_gather(comm, local)),
+                                 H(reference_all_gather(comm, local)))
+        comm.barrier()
+        q.put((rank, bool(ok), None))
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+
+
+def _run(target, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, tb in res:
+        assert ok, tb
+
+
+def test_two_processes_ipc_pull_decode():
+    _run(_p2p_worker)
+
+
 def test_two_processes_share_gpu():
     world = 2
     ctx = mp.get_context("spawn")
