@@ -264,6 +264,7 @@ def run_ours(args):
         launches_per_step = 5          # stats, finalize, encode pass 1 + fix-up, decode
     else:
         comm = coll.Communicator.from_process_group()
+        comm.use_p2p = args.transport == "p2p"
 
         def step(rec=False):
             return coll.zip_all_gather(comm, shard)
@@ -328,7 +329,8 @@ def run_ours(args):
         dist.all_reduce(rt, op=dist.ReduceOp.MAX)
         raw_ms = float(rt.item())
         raw = {"value": total_bytes / (raw_ms / 1e3) / 1e9, "ms_per_step": raw_ms,
-               "backend": args.backend, "speedup_zip_over_raw": raw_ms / ms}
+               "backend": args.backend, "transport": args.transport,
+               "speedup_zip_over_raw": raw_ms / ms}
 
     # ---- roofline of the dominant kernel (decode) ---------------------------
     roof = None
@@ -414,6 +416,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-settle", type=float, default=1.0)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="nccl: frames move with NCCL collectives, decode after arrival; "
+                         "p2p: decoder pulls peer frames over NVLink (IPC symmetric buffers)")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode: every rank on cuda:0 (use with --backend gloo)")
     args = ap.parse_args()
