@@ -78,6 +78,21 @@ int zc_encode(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
               uint8_t* frames, void* ws, int64_t ws_bytes, uint64_t* frame_len_dev,
               void* stream);
 
+/* Replaces container.serialize(codec.compress(x, codec.codebook_for(x)))
+ * (codec.py:164-185 + :264-305) — and for nseg > 1 the whole of
+ * collectives._prepare_frames (collectives.py:230-242): ONE codebook measured
+ * over the concatenation of the segments, one frame per segment.  flags bit 0
+ * selects the speculative path for large inputs (codebook guessed from a 1/32
+ * tile sample, exact statistic fused into the encoder, re-encode only if the
+ * exact codebook differs) — identical output, one fewer pass over x, but on
+ * B200 the fused encoder is issue-bound and slower, so it is opt-in.
+ * book_dev / result_dev receive the exact codebook and (sigma, finite count,
+ * path) like zc_codebook_measured. */
+int zc_encode_measured(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
+                       const int64_t* frame_off, int nseg, int gs_log2, uint8_t* frames, void* ws,
+                       int64_t ws_bytes, uint64_t* frame_len_dev, uint8_t* book_dev,
+                       double* result_dev, int flags, void* stream);
+
 /* Replaces codec.decompress(container.parse(frame)) (container.py:113-180,
  * codec.py:210-327) per segment, i.e. collectives._parse_peer_frame
  * (collectives.py:185-200).  stat[i] = frame start (16-byte aligned, may be a

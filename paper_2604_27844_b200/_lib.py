@@ -40,6 +40,8 @@ EXPORTS = {
     "zc_codebook_modal": (_int, [_vp, _P(_i64), _P(_i64), _int, _vp, _i64, _vp, _vp]),
     "zc_encode": (_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _int, _vp, _int, _vp, _vp, _i64,
                          _vp, _vp]),
+    "zc_encode_measured": (_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _int, _int, _vp, _vp, _i64,
+                                  _vp, _vp, _vp, _int, _vp]),
     "zc_decode": (_int, [_P(_vp), _P(_vp), _P(_i64), _P(_i64), _P(_i64), _int, _vp, _vp, _vp,
                          _i64, _int, _vp]),
     "zc_ipc_handle_bytes": (_int, []),

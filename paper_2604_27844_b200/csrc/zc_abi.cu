@@ -13,6 +13,8 @@ cudaError_t launch_encode(const uint16_t*, const EncodeSegs&, const uint8_t*, ui
                           uint64_t*, cudaStream_t);
 cudaError_t launch_decode(const DecodeSegs&, uint16_t*, int32_t*, void*, int, cudaStream_t);
 int64_t encode_workspace_bytes(int64_t ntiles);
+cudaError_t launch_encode_auto(const uint16_t*, const EncodeSegs&, const StatSegs&, int64_t,
+                               uint8_t*, void*, uint64_t*, uint8_t*, double*, int, cudaStream_t);
 }  // namespace zc
 
 using namespace zc;
@@ -129,6 +131,37 @@ int zc_encode(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
   }
   if (encode_workspace_bytes(s.tile_start[nseg]) > ws_bytes) return kStatusWorkspace;
   return status_of(launch_encode(x, s, book_dev, frames, ws, frame_len_dev, stream));
+}
+
+int zc_encode_measured(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
+                       const int64_t* frame_off, int nseg, int gs_log2, uint8_t* frames, void* ws,
+                       int64_t ws_bytes, uint64_t* frame_len_dev, uint8_t* book_dev,
+                       double* result_dev, int flags, cudaStream_t stream) {
+  if (nseg < 1 || nseg > kMaxSegments || !x || !book_dev || !result_dev || !frames || !ws ||
+      !frame_len_dev)
+    return kStatusBadArg;
+  if (gs_log2 < 0 || gs_log2 > 30) return kStatusBadArg;
+  EncodeSegs s{};
+  StatSegs ss{};
+  s.nseg = nseg;
+  ss.nseg = nseg;
+  s.gs_log2 = gs_log2;
+  int64_t total = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (seg_n[i] < 1 || seg_off[i] < 0 || frame_off[i] < 0) return kStatusBadArg;
+    if ((reinterpret_cast<uintptr_t>(frames + frame_off[i]) & (kAlign - 1)) != 0) return kStatusBadArg;
+    if (layout_of(seg_n[i], gs_log2).off[5] > int64_t(0xFFFFFFFF)) return kStatusTooLarge;
+    s.x_off[i] = ss.x_off[i] = seg_off[i];
+    s.n[i] = ss.n[i] = seg_n[i];
+    s.frame_off[i] = frame_off[i];
+    s.tile_start[i + 1] = ss.tile_start[i + 1] = s.tile_start[i] + tiles_of(seg_n[i]);
+    total += seg_n[i];
+  }
+  if (encode_workspace_bytes(s.tile_start[nseg]) > ws_bytes ||
+      128 + 32 * s.tile_start[nseg] > ws_bytes)
+    return kStatusWorkspace;
+  return status_of(launch_encode_auto(x, s, ss, total, frames, ws, frame_len_dev, book_dev,
+                                      result_dev, flags & 1, stream));
 }
 
 int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64_t* dyn_len,

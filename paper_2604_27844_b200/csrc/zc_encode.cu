@@ -17,7 +17,7 @@
 //   elements accumulate into one register whose bytes are plane0/1/2/escape
 //   group_index / escapes placed by the look-back prefix.
 // Bytes per element: 2 read + ~1.40 written (HBM bound, no tensor cores).
-#include "zc_common.cuh"
+#include "zc_stats.cuh"
 
 namespace zc {
 
@@ -319,7 +319,10 @@ __device__ __forceinline__ void encode_issue(const uint16_t* xs, int64_t n, int6
 __global__ void __launch_bounds__(kThreads)
 encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const RunPlan rp,
                     const uint8_t* __restrict__ book, uint8_t* __restrict__ frames,
-                    uint8_t* __restrict__ scratch, uint64_t* __restrict__ run_total) {
+                    uint8_t* __restrict__ scratch, uint64_t* __restrict__ run_total,
+                    Partial* __restrict__ stat_out, const int* __restrict__ cond, int cond_want) {
+  // conditional launch (speculative path): run only if *cond == cond_want
+  if (cond != nullptr && *cond != cond_want) return;
   extern __shared__ __align__(128) uint8_t s_dyn[];
   uint8_t* ring = s_dyn;                                              // kStages x 8 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kStages * kStageBytes);
@@ -358,6 +361,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
   __syncthreads();
 
   uint32_t run = 0;   // escapes of this run before the current tile
+  StatAcc acc;        // fused exact statistics (speculative-codebook path)
   // ---- lean loop: aligned input, tile fully inside the segment ---------------
   const int64_t t_full_end = aligned ? ((n / kTile) < t_end ? (n / kTile) : t_end) : t_begin;
   const int nfast = (int)(t_full_end > t_begin ? t_full_end - t_begin : 0);
@@ -374,6 +378,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
       const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
       const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      if (stat_out) acc.add16(w, 0xFFFFu);
       uint32_t sm[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -480,6 +485,8 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
         w[j] = lo | (hi << 16);
       }
     }
+    if (stat_out)
+      acc.add16(w, nvalid >= kEPT ? 0xFFFFu : (nvalid > 0 ? ((1u << nvalid) - 1u) : 0u));
 
     // ---- sign-mantissa bytes (codec.py:279) ---------------------------------
     uint32_t sm[4];
@@ -583,13 +590,16 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     }
   }
   if (tid == 0) run_total[blockIdx.x] = run;
+  if (stat_out) stat_block_finish(acc, stat_out + blockIdx.x);
 }
 
 // Pass 2: one CTA per pass-1 run.
 __global__ void __launch_bounds__(kThreads)
 encode_fixup_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __restrict__ book,
                     uint8_t* __restrict__ frames, const uint8_t* __restrict__ scratch,
-                    const uint64_t* __restrict__ run_total, uint64_t* __restrict__ frame_len) {
+                    const uint64_t* __restrict__ run_total, uint64_t* __restrict__ frame_len,
+                    const int* __restrict__ cond, int cond_want) {
+  if (cond != nullptr && *cond != cond_want) return;
   __shared__ uint64_t s_red[kWarps];
   __shared__ uint64_t s_off, s_zc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -702,8 +712,63 @@ static int grid_for(const void* fn, int threads, size_t dyn_smem) {
   return sms * (occ > 0 ? occ : 1);
 }
 
+constexpr int64_t kSpecArea = 512 * 1024;   // sampled + exact partials, guess book, flag
+
 int64_t encode_workspace_bytes(int64_t ntiles) {
-  return 256 + 8 * 4096 + (int64_t)kTile * ntiles;
+  return 256 + 8 * 4096 + kSpecArea + (int64_t)kTile * ntiles;
+}
+
+static RunPlan make_plan(const EncodeSegs& segs, int cap1) {
+  const int64_t ntiles = segs.tile_start[segs.nseg];
+  RunPlan rp{};
+  int runs = 0;
+  for (int s = 0; s < segs.nseg; ++s) {
+    const int64_t tiles = segs.tile_start[s + 1] - segs.tile_start[s];
+    int64_t want = (tiles * cap1 + ntiles - 1) / ntiles;
+    if (want < 1) want = 1;
+    if (want > tiles) want = tiles;
+    rp.run_start[s] = runs;
+    rp.tiles_per_run[s] = (tiles + want - 1) / want;
+    runs += (int)((tiles + rp.tiles_per_run[s] - 1) / rp.tiles_per_run[s]);
+  }
+  rp.run_start[segs.nseg] = runs;
+  rp.nruns = runs;
+  return rp;
+}
+
+static size_t tiles_dyn_smem() { return kStages * kStageBytes + kStages * sizeof(uint64_t); }
+
+static int tiles_cap() {
+  static int cap1 = 0;
+  if (cap1 == 0) {
+    cudaFuncSetAttribute(encode_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tiles_dyn_smem());
+    cap1 = grid_for((const void*)encode_tiles_kernel, kThreads, tiles_dyn_smem());
+    if (cap1 > 4096) cap1 = 4096;
+  }
+  return cap1;
+}
+
+// pass 1 + fix-up with optional fused statistics / conditional execution
+static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, const RunPlan& rp,
+                                   const uint8_t* book, uint8_t* frames, uint8_t* w8,
+                                   uint64_t* frame_len, Partial* stat_out, const int* cond,
+                                   int cond_want, cudaStream_t st) {
+  uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
+  uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea;
+  encode_tiles_kernel<<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
+      x, segs, rp, book, frames, scratch, run_total, stat_out, cond, cond_want);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_fixup(const EncodeSegs& segs, const RunPlan& rp, const uint8_t* book,
+                                uint8_t* frames, uint8_t* w8, uint64_t* frame_len,
+                                const int* cond, int cond_want, cudaStream_t st) {
+  uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
+  uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea;
+  encode_fixup_kernel<<<rp.nruns, kThreads, 0, st>>>(segs, rp, book, frames, scratch, run_total,
+                                                     frame_len, cond, cond_want);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8_t* book,
@@ -722,34 +787,62 @@ cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8
                                                        frame_len);
     return cudaGetLastError();
   }
-  const size_t dyn = kStages * kStageBytes + kStages * sizeof(uint64_t);
-  static int cap1 = 0;
-  if (cap1 == 0) {
-    cudaFuncSetAttribute(encode_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    cap1 = grid_for((const void*)encode_tiles_kernel, kThreads, dyn);
-    if (cap1 > 4096) cap1 = 4096;
+  const RunPlan rp = make_plan(segs, tiles_cap());
+  if (rp.nruns > 4096) return cudaErrorInvalidValue;
+  cudaError_t e = launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, nullptr, 0, st);
+  if (e != cudaSuccess) return e;
+  return launch_fixup(segs, rp, book, frames, w8, frame_len, nullptr, 0, st);
+}
+
+cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
+                                     double*, cudaStream_t);
+cudaError_t launch_codebook_sampled(const uint16_t*, const StatSegs&, int64_t, Partial*,
+                                    uint8_t*, double*, cudaStream_t);
+cudaError_t launch_finalize(const Partial*, int64_t, int64_t, uint8_t*, double*, const uint8_t*,
+                            int*, cudaStream_t);
+
+// Measured codebook + encode.  Large inputs take the speculative path: a
+// codebook guessed from every kSampleStride-th tile encodes while the encoder
+// accumulates the exact statistic; the exact codebook (reference
+// codebook_for semantics) is derived on the device and, only if it differs
+// from the guess, the frame is re-encoded (conditional kernels that return
+// immediately otherwise).  Saves the separate 2n-byte statistics pass.
+constexpr int64_t kSpecMinTiles = 1024;
+constexpr int64_t kSampleStride = 32;
+
+cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const StatSegs& ss,
+                               int64_t total, uint8_t* frames, void* ws, uint64_t* frame_len,
+                               uint8_t* book, double* result, int speculative, cudaStream_t st) {
+  // Measured (B200, 2^28): the fused f64 statistic makes the issue-bound
+  // encoder slower than the separate 2n-byte pass, so the two-step path is
+  // the default and the speculative path is opt-in (flags bit 0).
+  const int64_t ntiles = segs.tile_start[segs.nseg];
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
+  if (!speculative || ntiles < kSpecMinTiles) {
+    cudaError_t e = launch_codebook_measured(x, ss, total, ws, book, result, st);
+    if (e != cudaSuccess) return e;
+    return launch_encode(x, segs, book, frames, ws, frame_len, st);
   }
-  // split the resident CTAs over segments in proportion to their tiles
-  RunPlan rp{};
-  int runs = 0;
-  for (int s = 0; s < segs.nseg; ++s) {
-    const int64_t tiles = segs.tile_start[s + 1] - segs.tile_start[s];
-    int64_t want = (tiles * cap1 + ntiles - 1) / ntiles;
-    if (want < 1) want = 1;
-    if (want > tiles) want = tiles;
-    rp.run_start[s] = runs;
-    rp.tiles_per_run[s] = (tiles + want - 1) / want;
-    runs += (int)((tiles + rp.tiles_per_run[s] - 1) / rp.tiles_per_run[s]);
-  }
-  rp.run_start[segs.nseg] = runs;
-  rp.nruns = runs;
-  if (runs > 4096) return cudaErrorInvalidValue;
-  uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
-  uint8_t* scratch = w8 + 256 + 8 * 4096;
-  encode_tiles_kernel<<<runs, kThreads, dyn, st>>>(x, segs, rp, book, frames, scratch, run_total);
-  encode_fixup_kernel<<<runs, kThreads, 0, st>>>(segs, rp, book, frames, scratch, run_total,
-                                                 frame_len);
-  return cudaGetLastError();
+  const RunPlan rp = make_plan(segs, tiles_cap());
+  if (rp.nruns > 4096) return cudaErrorInvalidValue;
+  uint8_t* spec = w8 + 256 + 8 * 4096;
+  Partial* parts_guess = reinterpret_cast<Partial*>(spec);                  // <= 4096
+  Partial* parts_exact = reinterpret_cast<Partial*>(spec + 4096 * 32);      // <= 4096
+  uint8_t* guess = spec + 8192 * 32;
+  double* guess_res = reinterpret_cast<double*>(spec + 8192 * 32 + 64);
+  int* mismatch = reinterpret_cast<int*>(spec + 8192 * 32 + 128);
+  cudaError_t e = launch_codebook_sampled(x, ss, kSampleStride, parts_guess, guess, guess_res, st);
+  if (e != cudaSuccess) return e;
+  e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, parts_exact, nullptr, 0, st);
+  if (e != cudaSuccess) return e;
+  e = launch_finalize(parts_exact, rp.nruns, total, book, result, guess, mismatch, st);
+  if (e != cudaSuccess) return e;
+  e = launch_fixup(segs, rp, guess, frames, w8, frame_len, mismatch, 0, st);
+  if (e != cudaSuccess) return e;
+  // rare: the guess was wrong -> encode again with the exact codebook
+  e = launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, mismatch, 1, st);
+  if (e != cudaSuccess) return e;
+  return launch_fixup(segs, rp, book, frames, w8, frame_len, mismatch, 1, st);
 }
 
 }  // namespace zc

@@ -25,52 +25,18 @@
 // an explicit sigma that is 0 / negative / non-finite (reference codec.py:179-185
 // over arbitrary data).
 #include <cmath>
-#include "zc_common.cuh"
+#include "zc_stats.cuh"
 
 namespace zc {
 
-struct Partial {   // 32 B per CTA
-  double count;    // finite elements
-  double mean;
-  double m2;
-  double aux;      // exponent of some finite element (or -1)
-};
-
-__device__ __forceinline__ void chan_merge(double& na, double& ma, double& m2a, double nb,
-                                           double mb, double m2b) {
-  if (nb == 0.0) return;
-  if (na == 0.0) { na = nb; ma = mb; m2a = m2b; return; }
-  const double n = na + nb;
-  const double d = mb - ma;
-  ma = ma + d * (nb / n);
-  m2a = m2a + m2b + d * d * (na * nb / n);
-  na = n;
-}
-
-// Persistent: each CTA strides over tiles, each thread keeps running f64
-// sums of d = x - K (K = the first finite value the thread sees; non-finite
-// words are replaced by K so they add exactly 0) and the per-thread
-// (count, mean, M2) are Chan-merged once per CTA at the end.
-__device__ __forceinline__ void chan_shfl(double& n, double& m, double& q, int o) {
-  const double nb = __shfl_xor_sync(0xffffffffu, n, o);
-  const double mb = __shfl_xor_sync(0xffffffffu, m, o);
-  const double qb = __shfl_xor_sync(0xffffffffu, q, o);
-  chan_merge(n, m, q, nb, mb, qb);
-}
-
+// Persistent: each CTA strides over tiles (every `stride`-th tile: 1 for the
+// exact statistic, >1 for the sampled guess of the speculative encoder).
 __global__ void __launch_bounds__(kThreads)
-stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, Partial* __restrict__ out) {
-  __shared__ double s_n[kWarps], s_m[kWarps], s_q[kWarps];
-  __shared__ int s_e[kWarps];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t stride,
+             Partial* __restrict__ out) {
+  const int tid = threadIdx.x;
   const int64_t ntiles = segs.tile_start[segs.nseg];
-
-  bool have_k = false;
-  uint32_t kword = 0;        // K as a bf16 word in the high half of an f32
-  double K = 0.0, s1 = 0.0, s2 = 0.0;
-  uint64_t cnt = 0;
-  int kexp = -1;
-
+  StatAcc acc;
   uint32_t w[8], nw[8];
   auto load = [&](int64_t tile, uint32_t* dst) {
     const int s = find_seg(segs.tile_start, segs.nseg, tile);
@@ -91,78 +57,17 @@ stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, Partial* __res
       }
     }
   };
-  int64_t tile = blockIdx.x;
-  if (tile < ntiles) load(tile, w);
-  while (tile < ntiles) {
-    const int64_t nt = tile + gridDim.x;
-    if (nt < ntiles) load(nt, nw);
-    // finite test per half: exponent field != 255 (bf16.py:100 np.isfinite);
-    // bit 15 / bit 31 of v set iff the low / high word is finite
-    uint32_t v[8], allfin = 0x80008000u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      v[k] = (~w[k] & 0x7F807F80u) + 0x7F807F80u;
-      allfin &= v[k];
-    }
-    if (allfin == 0x80008000u && have_k) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double lo = (double)__uint_as_float(w[k] << 16) - K;
-        const double hi = (double)__uint_as_float(w[k] & 0xFFFF0000u) - K;
-        s1 += lo;
-        s2 = fma(lo, lo, s2);
-        s1 += hi;
-        s2 = fma(hi, hi, s2);
-      }
-      cnt += kEPT;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const uint32_t word = (k & 1) ? (w[k >> 1] >> 16) : (w[k >> 1] & 0xFFFFu);
-        const bool fin = (v[k >> 1] >> ((k & 1) ? 31 : 15)) & 1u;
-        if (fin && !have_k) {
-          have_k = true;
-          kword = word;
-          K = (double)__uint_as_float(word << 16);
-          kexp = (word >> 7) & 0xFF;
-        }
-        if (fin) {
-          const double d = (double)__uint_as_float(word << 16) - K;
-          s1 += d;
-          s2 = fma(d, d, s2);
-          ++cnt;
-        }
-      }
-    }
-    tile = nt;
+  int64_t i = blockIdx.x;
+  if (i * stride < ntiles) load(i * stride, w);
+  while (i * stride < ntiles) {
+    const int64_t ni = i + gridDim.x;
+    if (ni * stride < ntiles) load(ni * stride, nw);
+    acc.add16(w, 0xFFFFu);
+    i = ni;
 #pragma unroll
     for (int k = 0; k < 8; ++k) w[k] = nw[k];
   }
-  (void)kword;
-  // per-thread (count, mean, M2), then Chan merge: warp tree, then warps
-  double c = (double)cnt, m = 0.0, q = 0.0;
-  if (cnt > 0) {
-    m = K + s1 / c;
-    q = fmax(s2 - s1 * (s1 / c), 0.0);
-  }
-  int e = kexp;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    chan_shfl(c, m, q, o);
-    const int eb = __shfl_xor_sync(0xffffffffu, e, o);
-    e = (e < 0) ? eb : e;
-  }
-  if (lane == 0) { s_n[warp] = c; s_m[warp] = m; s_q[warp] = q; s_e[warp] = e; }
-  __syncthreads();
-  if (tid == 0) {
-    double na = 0.0, ma = 0.0, qa = 0.0;
-    int ea = -1;
-    for (int i = 0; i < kWarps; ++i) {
-      chan_merge(na, ma, qa, s_n[i], s_m[i], s_q[i]);
-      if (ea < 0) ea = s_e[i];
-    }
-    out[blockIdx.x] = Partial{na, ma, qa, (double)ea};
-  }
+  stat_block_finish(acc, out + blockIdx.x);
 }
 
 // --- host-identical codebook math (codec.py:74-161) ---------------------------
@@ -189,7 +94,8 @@ __device__ void write_window(uint8_t* book, int base) {
 // (1 analytic, 2 modal), book = 7 entries.
 __global__ void __launch_bounds__(1024)
 finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total_words,
-                uint8_t* __restrict__ book, double* __restrict__ result) {
+                uint8_t* __restrict__ book, double* __restrict__ result,
+                const uint8_t* __restrict__ guess, int* __restrict__ mismatch) {
   __shared__ double s_n[1024], s_m[1024], s_q[1024];
   __shared__ int s_e[1024];
   const int t = threadIdx.x;
@@ -236,6 +142,11 @@ finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total
       write_window(book, all_zero_exp ? -6 : mode - 127 - 3);
       result[2] = 2.0;
     }
+    if (mismatch) {
+      int diff = 0;
+      for (int i = 0; i < 7; ++i) diff |= (book[i] != guess[i]);
+      *mismatch = diff;
+    }
   }
 }
 
@@ -279,8 +190,8 @@ cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, in
     grid_cap = sms * (occ > 0 ? occ : 1);
   }
   const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
-  if (grid > 0) stats_kernel<<<(unsigned)grid, kThreads, 0, st>>>(x, segs, parts);
-  finalize_kernel<<<1, 1024, 0, st>>>(parts, grid, total, book, result);
+  if (grid > 0) stats_kernel<<<(unsigned)grid, kThreads, 0, st>>>(x, segs, 1, parts);
+  finalize_kernel<<<1, 1024, 0, st>>>(parts, grid, total, book, result, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -292,6 +203,34 @@ cudaError_t launch_codebook_modal(const uint16_t* x, const StatSegs& segs, int64
   if (e != cudaSuccess) return e;
   if (ntiles > 0) hist_kernel<<<(unsigned)ntiles, kThreads, 0, st>>>(x, segs, hist);
   mode_kernel<<<1, 32, 0, st>>>(hist, total, book);
+  return cudaGetLastError();
+}
+
+// Sampled guess for the speculative encoder: every `stride`-th tile.
+cudaError_t launch_codebook_sampled(const uint16_t* x, const StatSegs& segs, int64_t stride,
+                                    Partial* parts, uint8_t* book, double* result,
+                                    cudaStream_t st) {
+  const int64_t ntiles = segs.tile_start[segs.nseg];
+  const int64_t sampled = (ntiles + stride - 1) / stride;
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stats_kernel, kThreads, 0);
+    grid_cap = sms * (occ > 0 ? occ : 1);
+  }
+  const int64_t grid = sampled < grid_cap ? sampled : grid_cap;
+  stats_kernel<<<(unsigned)grid, kThreads, 0, st>>>(x, segs, stride, parts);
+  finalize_kernel<<<1, 1024, 0, st>>>(parts, grid, 0, book, result, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+// Exact codebook from per-CTA partials; flags a mismatch with `guess`.
+cudaError_t launch_finalize(const Partial* parts, int64_t nparts, int64_t total, uint8_t* book,
+                            double* result, const uint8_t* guess, int* mismatch,
+                            cudaStream_t st) {
+  finalize_kernel<<<1, 1024, 0, st>>>(parts, nparts, total, book, result, guess, mismatch);
   return cudaGetLastError();
 }
 

@@ -110,6 +110,31 @@ def encode(words: torch.Tensor, segs, book: torch.Tensor, gs_log2: int,
     return frame_len
 
 
+def encode_measured(words: torch.Tensor, segs, gs_log2: int, frames: torch.Tensor, frame_offs,
+                    frame_len: torch.Tensor | None = None, stream=None,
+                    speculative: bool = False):
+    """codebook_for over the concatenated segments + one frame per segment
+    (speculative fused statistics for large inputs).  Returns (book uint8[8],
+    result float64[3], frame_len int64[nseg]); all stay on the device."""
+    segs = list(segs)
+    nseg = len(segs)
+    if nseg > _lib.MAX_SEGMENTS:
+        raise ValueError("too many segments for one measured encode")
+    dev = words.device
+    if frame_len is None:
+        frame_len = torch.empty(nseg, dtype=torch.int64, device=dev)
+    book = torch.empty(8, dtype=torch.uint8, device=dev)
+    result = torch.empty(3, dtype=torch.float64, device=dev)
+    total = sum(n for _, n in segs)
+    ws = workspace(total, nseg, dev)
+    check(lib().zc_encode_measured(
+        words.data_ptr(), i64s(o for o, _ in segs), i64s(n for _, n in segs), i64s(frame_offs),
+        nseg, int(gs_log2), frames.data_ptr(), ws.data_ptr(), ws.numel(), frame_len.data_ptr(),
+        book.data_ptr(), result.data_ptr(), 1 if speculative else 0, stream_ptr(stream)),
+        "zc_encode_measured")
+    return book, result, frame_len
+
+
 def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_offs,
            write_out: bool = True, err: torch.Tensor | None = None, stream=None,
            device=None, large_groups: bool = False) -> torch.Tensor:

@@ -239,3 +239,61 @@ def test_unaligned_segments_and_batched_frames(golden_meta, golden_a2a):
         for k, q in enumerate(peers):
             got = host[foffs[k]:foffs[k] + flen[k]].tobytes()
             assert got == golden_a2a[f"r{rank}_f{q}"].tobytes(), (rank, q)
+
+
+def _measured_frame(x):
+    n = x.numel()
+    frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    book, res, flen = engine.encode_measured(x, [(0, n)], 9, frames, [0], speculative=True)
+    return bytes(frames[:int(flen.item())].cpu().numpy()), tuple(book[:7].tolist()), res.cpu()
+
+
+@pytest.mark.parametrize("case", ["gauss", "sample_fools_guess", "constant", "nan_heavy",
+                                  "outliers"])
+def test_speculative_measured_encode_is_exact(case):
+    n = 4096 * 1500 + 77          # above the speculative threshold (1024 tiles)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    v = torch.randn(n, device="cuda", generator=g)
+    if case == "gauss":
+        v = v * 0.02
+    elif case == "sample_fools_guess":
+        # every 32nd tile (the sampled ones) tiny, the rest large: guess != exact
+        v = v * 1000.0
+        t = torch.arange(n, device="cuda") // 4096
+        v[(t % 32) == 0] *= 1e-6
+    elif case == "constant":
+        v = torch.full((n,), 1.5, device="cuda")
+    elif case == "nan_heavy":
+        v = v * 3.0
+        v[::3] = float("nan")
+    elif case == "outliers":
+        v = v * 1e-3
+        v[::997] *= 1e4
+    x = engine.words_view(v.to(torch.bfloat16))
+    frame, book, res = _measured_frame(x)
+    ref_book = zc.codebook_for(x)
+    assert book == ref_book.entries
+    assert frame == zc.serialize(zc.compress(x, ref_book))
+    host = x.cpu().numpy().view(np.uint16)
+    assert book == zo.book_for(host)
+
+
+def test_speculative_multi_segment_matches_prepare_frames(golden_meta):
+    # per-peer frames of an all-to-all, sizes above the threshold
+    rng = np.random.default_rng(3)
+    sizes = [4096 * 400 + 13, 0, 4096 * 700 + 5, 4096 * 100]
+    chunks = [zo.from_f64(rng.standard_normal(c) * 0.5) for c in sizes]
+    buf = np.concatenate(chunks)
+    offs = np.concatenate([[0], np.cumsum(sizes)])[:-1]
+    x = torch.from_numpy(buf.view(np.int16)).cuda()
+    segs = [(int(offs[q]), sizes[q]) for q in range(4) if q != 1 and sizes[q]]
+    caps = [engine.max_frame_bytes(c) for _, c in segs]
+    foffs = np.concatenate([[0], np.cumsum(caps)])[:-1]
+    frames = torch.empty(int(sum(caps)), dtype=torch.uint8, device="cuda")
+    book, _, flen = engine.encode_measured(x, segs, 9, frames, [int(f) for f in foffs],
+                                           speculative=True)
+    expect = zo.peer_frames(chunks, rank=1)
+    host = frames.cpu().numpy()
+    fl = flen.cpu().tolist()
+    for k, q in enumerate([0, 2, 3]):
+        assert host[foffs[k]:foffs[k] + fl[k]].tobytes() == expect[q], q
