@@ -299,7 +299,10 @@ def zip_all_to_all_d2(comm: Communicator, spec: AlltoAllSpec,
                       sigma: float | None = None) -> list:
     """Design 2 (collectives.py:281-325): static sections first (receivers
     pre-size them from recv_counts), then dynamic sizes, then dynamic
-    sections; frames are decoded from the split receive buffers in place."""
+    sections; frames are decoded from the split receive buffers in place.
+    With ``comm.use_p2p`` the peer-memory pull-decode path is used instead."""
+    if getattr(comm, "use_p2p", False):
+        return zip_all_to_all_p2p(comm, spec, sigma)
     _check_world(comm, spec.world_size)
     dev = _dev(comm)
     if comm.world_size == 1:
@@ -420,3 +423,77 @@ def zip_all_gather_p2p(comm: Communicator, local, sigma: float | None = None) ->
         raise CollectiveError("peer frame never became ready (timeout)")
     _raise_decode_errors(err, peers)
     return out
+
+
+def _a2a_layout(counts_row: list, sender: int) -> list:
+    """Frame offsets inside `sender`'s symmetric buffer: peers in rank order,
+    capacity max_frame_bytes(count) each (a pure function of the counts, so
+    every rank derives every sender's layout without exchanging offsets)."""
+    offs, pos = [0] * len(counts_row), 0
+    for q, c in enumerate(counts_row):
+        offs[q] = pos
+        if q != sender and c:
+            pos += engine.max_frame_bytes(c, GS_LOG2)
+    return offs + [pos]
+
+
+def zip_all_to_all_p2p(comm: Communicator, spec: AlltoAllSpec,
+                       sigma: float | None = None) -> list:
+    """All-to-all where the transfer IS the decode (MoE dispatch/combine):
+    one batched K4 launch encodes every peer frame into this rank's symmetric
+    buffer, peers are signalled device-side, and one batched K3 launch pulls
+    this rank's frame from every peer's HBM over NVLink and decodes it in
+    place.  Results identical to reference_all_to_all."""
+    from .peer import workspace_for
+    _check_world(comm, spec.world_size)
+    dev = _dev(comm)
+    W, me = comm.world_size, comm.rank
+    if W == 1:
+        return [device_words(spec.send_chunks[0], dev).clone()]
+    buf, offs, counts = _pack(spec.send_chunks, dev)
+    # the full count matrix: protocol check + every sender's layout
+    if isinstance(comm, HubCommunicator):
+        matrix = comm._post_and_collect(list(counts))
+    else:
+        import torch.distributed as dist
+        rows = [None] * W
+        dist.all_gather_object(rows, list(counts), group=comm.group)
+        matrix = rows
+    for p in comm.peers():
+        if matrix[p][me] != spec.recv_counts[p]:
+            raise ProtocolError(f"rank {p} will send {matrix[p][me]} elements, "
+                                f"rank {me} expected {spec.recv_counts[p]}")
+    layouts = [_a2a_layout(matrix[p], p) for p in range(W)]
+    ws = workspace_for(comm, max(lay[-1] for lay in layouts) + 128)
+    e = ws.epoch + 1
+    ws.epoch = e
+    werr = torch.full((1,), engine.ERR_OK, dtype=torch.int32, device=dev)
+    if e > 1:
+        ws.wait(1, e - 1, werr)
+    peers_out = [q for q in comm.peers() if counts[q]]
+    if peers_out:
+        segs = [(offs[q], counts[q]) for q in peers_out]
+        if sigma is not None and math.isfinite(sigma) and sigma > 0.0:
+            book = codec.derive_codebook(sigma).device_tensor(dev)
+        else:
+            book = codec.device_codebook(buf, sigma, segs)
+        engine.encode(buf, segs, book, GS_LOG2, ws.buf,
+                      [256 + layouts[me][q] for q in peers_out])
+    ws.signal(0, e)
+    ws.wait(0, e, werr)
+    peers_in = [p for p in comm.peers() if spec.recv_counts[p]]
+    roffs = np.concatenate([[0], np.cumsum(spec.recv_counts)]).astype(np.int64)
+    flat = torch.empty(max(int(roffs[-1]), 1), dtype=torch.int16, device=dev)
+    err = None
+    if peers_in:
+        err = engine.decode([ws.peer_base[p] + 256 + layouts[p][me] for p in peers_in],
+                            [0] * len(peers_in), None, [spec.recv_counts[p] for p in peers_in],
+                            flat, [int(roffs[p]) for p in peers_in])
+    ws.signal(1, e)
+    result = [flat[int(roffs[p]):int(roffs[p]) + spec.recv_counts[p]] for p in range(W)]
+    result[me] = buf[offs[me]:offs[me] + counts[me]].clone()
+    if int(werr.item()) != engine.ERR_OK:
+        raise CollectiveError("peer frame never became ready (timeout)")
+    if err is not None:
+        _raise_decode_errors(err, peers_in)
+    return result

@@ -264,7 +264,7 @@ encode_lookback_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs,
 
 
 // ============================================================================
-// Two-kernel encoder for large inputs (the default above kLookbackMaxTiles).
+// Run-based encoder for large inputs (the default above kLookbackMaxTiles).
 //
 // Pass 1 (encode_tiles_kernel) is the HBM-bound part and has no inter-CTA
 // dependence.  Persistent CTAs each own a contiguous run of tiles of one
@@ -273,10 +273,11 @@ encode_lookback_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs,
 // per CTA are loading while one is encoded.  The CTA writes the sign-mantissa
 // and plane sections in place, group_index entries relative to its own run,
 // its escapes compacted into its scratch run, and its escape total.
-// Pass 2 (encode_fixup_kernel, one CTA per pass-1 CTA) sums the totals of
-// the runs before it (<= a few hundred values), adds that offset to its
-// group_index entries, moves its escapes to their final place with
-// coalesced copies, and the segment's last run writes header + pads.
+// Its epilogue resolves the run's escape offset with a one-shot decoupled
+// look-back over the runs of the segment (every CTA is resident and
+// publishes its total before waiting), adds the offset to the run's
+// group_index entries, moves the run's escapes to their final place, and
+// the segment's last run writes header + pads -- no second kernel.
 // Extra traffic: 2 x zero_count bytes (the scratch round trip).
 // ============================================================================
 
@@ -320,7 +321,8 @@ __global__ void __launch_bounds__(kThreads)
 encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const RunPlan rp,
                     const uint8_t* __restrict__ book, uint8_t* __restrict__ frames,
                     uint8_t* __restrict__ scratch, uint64_t* __restrict__ run_total,
-                    Partial* __restrict__ stat_out, const int* __restrict__ cond, int cond_want) {
+                    Partial* __restrict__ stat_out, const int* __restrict__ cond, int cond_want,
+                    uint64_t* __restrict__ run_status, uint64_t* __restrict__ frame_len) {
   // conditional launch (speculative path): run only if *cond == cond_want
   if (cond != nullptr && *cond != cond_want) return;
   extern __shared__ __align__(128) uint8_t s_dyn[];
@@ -591,112 +593,41 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
   }
   if (tid == 0) run_total[blockIdx.x] = run;
   if (stat_out) stat_block_finish(acc, stat_out + blockIdx.x);
-}
+  if (run_status == nullptr) return;
 
-// Pass 2: one CTA per pass-1 run.
-__global__ void __launch_bounds__(kThreads)
-encode_fixup_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __restrict__ book,
-                    uint8_t* __restrict__ frames, const uint8_t* __restrict__ scratch,
-                    const uint64_t* __restrict__ run_total, uint64_t* __restrict__ frame_len,
-                    const int* __restrict__ cond, int cond_want) {
-  if (cond != nullptr && *cond != cond_want) return;
-  __shared__ uint64_t s_red[kWarps];
-  __shared__ uint64_t s_off, s_zc;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int seg;
-  int64_t t_begin, t_end;
-  run_range(segs, rp, blockIdx.x, seg, t_begin, t_end);
-  const int r0 = rp.run_start[seg], r1 = rp.run_start[seg + 1];
-  const bool last_run = (int)blockIdx.x == r1 - 1;
-  // offset of this run = sum of the totals of the earlier runs of the segment
-  uint64_t before = 0, all = 0;
-  for (int r = r0 + tid; r < r1; r += kThreads) {
-    const uint64_t v = run_total[r];
-    if (r < (int)blockIdx.x) before += v;
-    all += v;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    before += __shfl_xor_sync(0xffffffffu, before, o);
-    all += __shfl_xor_sync(0xffffffffu, all, o);
-  }
-  if (lane == 0) s_red[warp] = before;
-  __syncthreads();
-  if (tid == 0) {
-    uint64_t b = 0;
-    for (int i = 0; i < kWarps; ++i) b += s_red[i];
-    s_off = b;
-  }
-  __syncthreads();
-  if (lane == 0) s_red[warp] = all;
-  __syncthreads();
-  if (tid == 0) {
-    uint64_t a = 0;
-    for (int i = 0; i < kWarps; ++i) a += s_red[i];
-    s_zc = a;
+  // ---- fused fix-up: escape offset of this run by a one-shot look-back over
+  // the runs of the segment (all CTAs are resident, each publishes its total
+  // before waiting), then finalize group_index, place escapes, header ------
+  __shared__ uint64_t s_off;
+  if (warp == 0) {
+    const uint64_t ex = lookback_warp(run_status, blockIdx.x, rp.run_start[seg], run, 0);
+    if (lane == 0) s_off = ex;
   }
   __syncthreads();
   const uint64_t P = s_off;
-  const int64_t n = segs.n[seg];
-  const int gsl = segs.gs_log2;
-  const Layout L = layout_of(n, gsl);
-  uint8_t* frame = frames + segs.frame_off[seg];
   if (t_begin < t_end) {
-    // group_index: add the run offset to every group starting inside the run
     const int64_t e0 = t_begin * kTile;
     const int64_t e1 = (t_end * kTile < n) ? t_end * kTile : n;
     const int64_t g0 = (e0 + (int64_t(1) << gsl) - 1) >> gsl;
     const int64_t g1 = (e1 + (int64_t(1) << gsl) - 1) >> gsl;
-    uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
-    for (int64_t g = g0 + tid; g < g1; g += kThreads) gi[g] += (uint32_t)P;
-    // escapes: scratch run -> dynamic section at P
-    const uint64_t cnt = run_total[blockIdx.x];
-    const uint8_t* src = scratch + (segs.tile_start[seg] + t_begin) * kTile;
+    if (P != 0)
+      for (int64_t g = g0 + tid; g < g1; g += kThreads) gi[g] += (uint32_t)P;
     uint8_t* dst = frame + L.off[5] + P;
-    // align the destination to 4 B, then move words assembled from bytes
     const uint32_t head = (uint32_t)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
-    const uint64_t h = cnt < head ? cnt : head;
-    if (tid < h) dst[tid] = src[tid];
-    const uint64_t body = (cnt - h) / 4;
+    const uint32_t h = run < head ? run : head;
+    if (tid < h) dst[tid] = esc_out[tid];
+    const uint32_t body = (run - h) / 4;
     uint32_t* dst4 = reinterpret_cast<uint32_t*>(dst + h);
-    for (uint64_t i = tid; i < body; i += kThreads) {
-      const uint8_t* q = src + h + 4 * i;
+    for (uint32_t i = tid; i < body; i += kThreads) {
+      const uint8_t* q = esc_out + h + 4 * i;
       dst4[i] = (uint32_t)q[0] | (uint32_t)q[1] << 8 | (uint32_t)q[2] << 16 | (uint32_t)q[3] << 24;
     }
-    for (uint64_t i = h + 4 * body + tid; i < cnt; i += kThreads) dst[i] = src[i];
+    for (uint32_t i = h + 4 * body + tid; i < run; i += kThreads) dst[i] = esc_out[i];
   }
-  if (last_run) {
-    const uint64_t zc = s_zc;
-    const int t = tid;
-    if (t < 128) {
-      uint8_t v = 0;
-      if (t < 4) v = "ZCCL"[t];
-      else if (t == 4) v = 1;
-      else if (t == 6) v = (uint8_t)gsl;
-      else if (t >= 8 && t < 16) v = (uint8_t)(uint64_t(n) >> (8 * (t - 8)));
-      else if (t >= 16 && t < 24) v = (uint8_t)(zc >> (8 * (t - 16)));
-      else if (t >= 24 && t < 31) v = book[t - 24];
-      else if (t == 31) v = book[0];
-      else if (t >= 32 && t < 56) {
-        const int i = (t - 32) >> 2;
-        int64_t o = 0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) o = (k == i) ? L.off[k] : o;
-        v = (uint8_t)(uint32_t(o) >> (8 * ((t - 32) & 3)));
-      }
-      frame[t] = v;
-    }
-#pragma unroll
-    for (int r = 0; r < 6; ++r) {
-      const int64_t end = r == 0 ? L.off[0] + n
-                        : r < 4 ? L.off[r] + L.plane_bytes
-                        : r == 4 ? L.off[4] + 4 * L.groups
-                                 : L.off[5] + (int64_t)zc;
-      const int64_t lim = r < 5 ? L.off[r + 1] : L.off[5] + pad128((int64_t)zc);
-      const int64_t p = end + t;
-      if (p < lim) frame[p] = 0;
-    }
-    if (t == 0) frame_len[seg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
+  if ((int)blockIdx.x == rp.run_start[seg + 1] - 1) {
+    const uint64_t zc = P + run;
+    write_header_and_pads(frame, L, zc, s_book);
+    if (tid == 0) frame_len[seg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
   }
 }
 
@@ -750,24 +681,20 @@ static int tiles_cap() {
 }
 
 // pass 1 + fix-up with optional fused statistics / conditional execution
+// pass 1 with the fused fix-up epilogue (run-level look-back); optional fused
+// statistics / conditional execution for the speculative path
 static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, const RunPlan& rp,
                                    const uint8_t* book, uint8_t* frames, uint8_t* w8,
                                    uint64_t* frame_len, Partial* stat_out, const int* cond,
                                    int cond_want, cudaStream_t st) {
   uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
+  uint64_t* run_status = reinterpret_cast<uint64_t*>(w8 + 256 + 8 * 4096 + kSpecArea - 8 * 4096);
   uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea;
+  cudaError_t e = cudaMemsetAsync(run_status, 0, 8 * (size_t)rp.nruns, st);
+  if (e != cudaSuccess) return e;
   encode_tiles_kernel<<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
-      x, segs, rp, book, frames, scratch, run_total, stat_out, cond, cond_want);
-  return cudaGetLastError();
-}
-
-static cudaError_t launch_fixup(const EncodeSegs& segs, const RunPlan& rp, const uint8_t* book,
-                                uint8_t* frames, uint8_t* w8, uint64_t* frame_len,
-                                const int* cond, int cond_want, cudaStream_t st) {
-  uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
-  uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea;
-  encode_fixup_kernel<<<rp.nruns, kThreads, 0, st>>>(segs, rp, book, frames, scratch, run_total,
-                                                     frame_len, cond, cond_want);
+      x, segs, rp, book, frames, scratch, run_total, stat_out, cond, cond_want, run_status,
+      frame_len);
   return cudaGetLastError();
 }
 
@@ -789,9 +716,7 @@ cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8
   }
   const RunPlan rp = make_plan(segs, tiles_cap());
   if (rp.nruns > 4096) return cudaErrorInvalidValue;
-  cudaError_t e = launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, nullptr, 0, st);
-  if (e != cudaSuccess) return e;
-  return launch_fixup(segs, rp, book, frames, w8, frame_len, nullptr, 0, st);
+  return launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, nullptr, 0, st);
 }
 
 cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
@@ -826,7 +751,7 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   const RunPlan rp = make_plan(segs, tiles_cap());
   if (rp.nruns > 4096) return cudaErrorInvalidValue;
   uint8_t* spec = w8 + 256 + 8 * 4096;
-  Partial* parts_guess = reinterpret_cast<Partial*>(spec);                  // <= 4096
+  Partial* parts_guess = reinterpret_cast<Partial*>(spec + 128);            // <= 4095 (counter at -64)
   Partial* parts_exact = reinterpret_cast<Partial*>(spec + 4096 * 32);      // <= 4096
   uint8_t* guess = spec + 8192 * 32;
   double* guess_res = reinterpret_cast<double*>(spec + 8192 * 32 + 64);
@@ -837,12 +762,8 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   if (e != cudaSuccess) return e;
   e = launch_finalize(parts_exact, rp.nruns, total, book, result, guess, mismatch, st);
   if (e != cudaSuccess) return e;
-  e = launch_fixup(segs, rp, guess, frames, w8, frame_len, mismatch, 0, st);
-  if (e != cudaSuccess) return e;
   // rare: the guess was wrong -> encode again with the exact codebook
-  e = launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, mismatch, 1, st);
-  if (e != cudaSuccess) return e;
-  return launch_fixup(segs, rp, book, frames, w8, frame_len, mismatch, 1, st);
+  return launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, mismatch, 1, st);
 }
 
 }  // namespace zc

@@ -29,45 +29,121 @@
 
 namespace zc {
 
-// Persistent: each CTA strides over tiles (every `stride`-th tile: 1 for the
-// exact statistic, >1 for the sampled guess of the speculative encoder).
+__device__ void finalize_block(const Partial* parts, int64_t nparts, int64_t total_words,
+                               uint8_t* book, double* result, const uint8_t* guess,
+                               int* mismatch);
+
+// Persistent: each CTA owns a contiguous run of tiles (every `stride`-th
+// tile of the concatenated segments: 1 for the exact statistic, >1 for the
+// sampled guess) and keeps a kSStages-deep ring of 8 KB tiles in flight with
+// TMA bulk copies; thread 0 issues, all threads accumulate.  The last CTA to
+// finish merges every partial in a fixed order and derives the codebook.
+constexpr int kSStages = 4;
+constexpr int kSStageBytes = kTile * 2;
+
+__device__ __forceinline__ void stats_issue(const uint16_t* x, const StatSegs& segs,
+                                            int64_t tile, uint8_t* stage, uint64_t* bar) {
+  const int s = find_seg(segs.tile_start, segs.nseg, tile);
+  const uint16_t* xs = x + segs.x_off[s];
+  const int64_t base = (tile - segs.tile_start[s]) * kTile;
+  const int64_t valid = segs.n[s] - base;
+  const uint32_t bytes = (uint32_t)((valid >= kTile ? kTile : valid) * 2) & ~15u;
+  if (((reinterpret_cast<uintptr_t>(xs) & 15) == 0) && bytes > 0) {
+    mbar_arrive_expect_tx(bar, bytes);
+    tma_load_1d(stage, xs + base, bytes, bar);
+  } else {
+    mbar_arrive(bar);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
 stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t stride,
-             Partial* __restrict__ out) {
+             Partial* __restrict__ out, unsigned* __restrict__ done, int64_t total_words,
+             uint8_t* __restrict__ book, double* __restrict__ result) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  uint8_t* ring = s_dyn;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kSStages * kSStageBytes);
   const int tid = threadIdx.x;
   const int64_t ntiles = segs.tile_start[segs.nseg];
+  const int64_t nsample = (ntiles + stride - 1) / stride;        // tiles this launch reads
+  const int64_t per = (nsample + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = blockIdx.x * per;
+  const int64_t i1 = (i0 + per < nsample) ? i0 + per : nsample;
+  if (tid == 0) {
+    for (int k = 0; k < kSStages; ++k) mbar_init(bars + k, 1);
+    fence_mbar_init();
+    for (int k = 0; k < kSStages && i0 + k < i1; ++k)
+      stats_issue(x, segs, (i0 + k) * stride, ring + k * kSStageBytes, bars + k);
+  }
+  __syncthreads();
   StatAcc acc;
-  uint32_t w[8], nw[8];
-  auto load = [&](int64_t tile, uint32_t* dst) {
-    const int s = find_seg(segs.tile_start, segs.nseg, tile);
-    const uint16_t* xs = x + segs.x_off[s];
-    const int64_t base = (tile - segs.tile_start[s]) * kTile + (int64_t)tid * kEPT;
-    const int64_t nvalid = segs.n[s] - base;
-    if (nvalid >= kEPT && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)) {
-      const uint4 a = ld_stream_v4(xs + base), b = ld_stream_v4(xs + base + 8);
-      dst[0] = a.x; dst[1] = a.y; dst[2] = a.z; dst[3] = a.w;
-      dst[4] = b.x; dst[5] = b.y; dst[6] = b.z; dst[7] = b.w;
+  for (int64_t i = i0; i < i1; ++i) {
+    const int k = (int)(i - i0);
+    const int st = k & (kSStages - 1);
+    const int64_t tile = i * stride;
+    const int sg = find_seg(segs.tile_start, segs.nseg, tile);
+    const uint16_t* xs = x + segs.x_off[sg];
+    const int64_t base = (tile - segs.tile_start[sg]) * kTile;
+    const int64_t tvalid = segs.n[sg] - base;
+    const int tma_elems = ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)
+        ? (int)((((tvalid >= kTile ? kTile : tvalid) * 2) & ~15) / 2) : 0;
+    mbar_wait(bars + st, (uint32_t)((k / kSStages) & 1));
+    const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kSStageBytes);
+    uint32_t w[8];
+    uint32_t valid = 0xFFFFu;
+    if (tid * kEPT + kEPT <= tma_elems) {
+      const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
+      const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
     } else {
+      const int64_t nvalid = tvalid - (int64_t)tid * kEPT;
+      valid = nvalid >= kEPT ? 0xFFFFu : (nvalid > 0 ? ((1u << nvalid) - 1u) : 0u);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        // out-of-range elements become NaN words: excluded like non-finite
-        const uint32_t lo = (2 * k < nvalid) ? xs[base + 2 * k] : 0x7FC0u;
-        const uint32_t hi = (2 * k + 1 < nvalid) ? xs[base + 2 * k + 1] : 0x7FC0u;
-        dst[k] = lo | (hi << 16);
+      for (int j = 0; j < 8; ++j) {
+        const int e0 = tid * kEPT + 2 * j;
+        uint32_t lo = 0, hi = 0;
+        if (2 * j < nvalid) lo = (e0 < tma_elems) ? tw[e0] : xs[base + e0];
+        if (2 * j + 1 < nvalid) hi = (e0 + 1 < tma_elems) ? tw[e0 + 1] : xs[base + e0 + 1];
+        w[j] = lo | (hi << 16);
       }
     }
-  };
-  int64_t i = blockIdx.x;
-  if (i * stride < ntiles) load(i * stride, w);
-  while (i * stride < ntiles) {
-    const int64_t ni = i + gridDim.x;
-    if (ni * stride < ntiles) load(ni * stride, nw);
-    acc.add16(w, 0xFFFFu);
-    i = ni;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = nw[k];
+    acc.add16(w, valid);
+    __syncthreads();                                   // stage free
+    if (tid == 0 && i + kSStages < i1) {
+      fence_proxy_async();
+      stats_issue(x, segs, (i + kSStages) * stride, ring + st * kSStageBytes, bars + st);
+    }
   }
   stat_block_finish(acc, out + blockIdx.x);
+  // the last CTA to finish merges every partial (fixed order) and derives the
+  // codebook: no separate finalize launch
+  __shared__ bool s_last;
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    finalize_block(out, gridDim.x, total_words, book, result, nullptr, nullptr);
+  }
+}
+
+static size_t stats_dyn_smem() { return kSStages * kSStageBytes + kSStages * sizeof(uint64_t); }
+
+static int stats_grid_cap() {
+  static int cap = 0;
+  if (cap == 0) {
+    cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stats_dyn_smem());
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stats_kernel, kThreads, stats_dyn_smem());
+    cap = sms * (occ > 0 ? occ : 1);
+  }
+  return cap;
 }
 
 // --- host-identical codebook math (codec.py:74-161) ---------------------------
@@ -92,38 +168,50 @@ __device__ void write_window(uint8_t* book, int base) {
 // fixed contiguous range, then a fixed binary tree.  result[0] = sigma
 // (NaN when no finite value), result[1] = finite count, result[2] = path
 // (1 analytic, 2 modal), book = 7 entries.
-__global__ void __launch_bounds__(1024)
-finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total_words,
-                uint8_t* __restrict__ book, double* __restrict__ result,
-                const uint8_t* __restrict__ guess, int* __restrict__ mismatch) {
-  __shared__ double s_n[1024], s_m[1024], s_q[1024];
-  __shared__ int s_e[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (nparts + 1023) / 1024;
+// Fixed-order merge of `nparts` partials by one kThreads-thread CTA, then the
+// reference derivation.  result[0] = sigma (NaN when no finite value),
+// result[1] = finite count, result[2] = path (1 analytic, 2 modal).  When
+// `mismatch` is given, *mismatch = (book != guess).
+__device__ void finalize_block(const Partial* parts, int64_t nparts, int64_t total_words,
+                               uint8_t* book, double* result, const uint8_t* guess,
+                               int* mismatch) {
+  __shared__ double f_n[kWarps], f_m[kWarps], f_q[kWarps];
+  __shared__ int f_e[kWarps];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t per = (nparts + kThreads - 1) / kThreads;
   double na = 0.0, ma = 0.0, qa = 0.0;
   int e = -1;
   for (int64_t i = t * per; i < (t + 1) * per && i < nparts; ++i) {
-    const Partial p = parts[i];
-    chan_merge(na, ma, qa, p.count, p.mean, p.m2);
-    if (e < 0) e = (int)p.aux;
+    const double c = __ldcg(&parts[i].count), m = __ldcg(&parts[i].mean);
+    const double q = __ldcg(&parts[i].m2), a = __ldcg(&parts[i].aux);
+    chan_merge(na, ma, qa, c, m, q);
+    if (e < 0) e = (int)a;
   }
-  s_n[t] = na; s_m[t] = ma; s_q[t] = qa; s_e[t] = e;
-  __syncthreads();
-  for (int s = 512; s > 0; s >>= 1) {
-    if (t < s) {
-      double a = s_n[t], b = s_m[t], c = s_q[t];
-      chan_merge(a, b, c, s_n[t + s], s_m[t + s], s_q[t + s]);
-      s_n[t] = a; s_m[t] = b; s_q[t] = c;
-      if (s_e[t] < 0) s_e[t] = s_e[t + s];
+  // fixed pairwise tree inside the warp (lane i absorbs lane i+o)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double nb = __shfl_down_sync(0xffffffffu, na, o);
+    const double mb = __shfl_down_sync(0xffffffffu, ma, o);
+    const double qb = __shfl_down_sync(0xffffffffu, qa, o);
+    const int eb = __shfl_down_sync(0xffffffffu, e, o);
+    if ((lane & (2 * o - 1)) == 0) {
+      chan_merge(na, ma, qa, nb, mb, qb);
+      if (e < 0) e = eb;
     }
-    __syncthreads();
   }
+  if (lane == 0) { f_n[warp] = na; f_m[warp] = ma; f_q[warp] = qa; f_e[warp] = e; }
+  __syncthreads();
   if (t == 0) {
-    const double cnt = s_n[0];
-    const double sigma = cnt > 0.0 ? sqrt(s_q[0] / cnt) : nan("");
+    double cn = 0.0, cm = 0.0, cq = 0.0;
+    int ce = -1;
+    for (int i = 0; i < kWarps; ++i) {
+      chan_merge(cn, cm, cq, f_n[i], f_m[i], f_q[i]);
+      if (ce < 0) ce = f_e[i];
+    }
+    const double sigma = cn > 0.0 ? sqrt(cq / cn) : nan("");
     result[0] = sigma;
-    result[1] = cnt;
-    if (cnt > 0.0 && isfinite(sigma) && sigma > 0.0) {
+    result[1] = cn;
+    if (cn > 0.0 && isfinite(sigma) && sigma > 0.0) {
       // derive_codebook (codec.py:149-161)
       const double xo = log2(sigma) + kBaseExponentOffset;
       const double lo = floor(xo), hi = ceil(xo);
@@ -132,13 +220,14 @@ finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total
       write_window(book, base);
       result[2] = 1.0;
     } else {
-      // modal fallback (codec.py:181-185) with the two possible bins
-      const double c_nf = (double)total_words - cnt;
+      // modal fallback (codec.py:181-185): with sigma 0 or no finite value the
+      // histogram has at most two bins, the common finite exponent and 255
+      const double c_nf = (double)total_words - cn;
       int mode;
-      if (cnt > 0.0 && cnt >= c_nf) mode = s_e[0];
+      if (cn > 0.0 && cn >= c_nf) mode = ce;
       else if (total_words > 0) mode = 255;
       else mode = 0;
-      const bool all_zero_exp = (mode == 0) && (cnt == (double)total_words);
+      const bool all_zero_exp = (mode == 0) && (cn == (double)total_words);
       write_window(book, all_zero_exp ? -6 : mode - 127 - 3);
       result[2] = 2.0;
     }
@@ -148,6 +237,13 @@ finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total
       *mismatch = diff;
     }
   }
+}
+
+__global__ void __launch_bounds__(kThreads)
+finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total_words,
+                uint8_t* __restrict__ book, double* __restrict__ result,
+                const uint8_t* __restrict__ guess, int* __restrict__ mismatch) {
+  finalize_block(parts, nparts, total_words, book, result, guess, mismatch);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -181,17 +277,17 @@ cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, in
                                      void* ws, uint8_t* book, double* result, cudaStream_t st) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
   Partial* parts = reinterpret_cast<Partial*>(reinterpret_cast<uint8_t*>(ws) + 128);
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stats_kernel, kThreads, 0);
-    grid_cap = sms * (occ > 0 ? occ : 1);
+  const int cap = stats_grid_cap();
+  const int64_t grid = ntiles < cap ? ntiles : cap;
+  unsigned* done = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(ws) + 64);
+  if (grid > 0) {
+    cudaError_t e = cudaMemsetAsync(done, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(x, segs, 1, parts, done,
+                                                                      total, book, result);
+  } else {
+    finalize_kernel<<<1, kThreads, 0, st>>>(parts, 0, total, book, result, nullptr, nullptr);
   }
-  const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
-  if (grid > 0) stats_kernel<<<(unsigned)grid, kThreads, 0, st>>>(x, segs, 1, parts);
-  finalize_kernel<<<1, 1024, 0, st>>>(parts, grid, total, book, result, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -212,17 +308,13 @@ cudaError_t launch_codebook_sampled(const uint16_t* x, const StatSegs& segs, int
                                     cudaStream_t st) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
   const int64_t sampled = (ntiles + stride - 1) / stride;
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stats_kernel, kThreads, 0);
-    grid_cap = sms * (occ > 0 ? occ : 1);
-  }
-  const int64_t grid = sampled < grid_cap ? sampled : grid_cap;
-  stats_kernel<<<(unsigned)grid, kThreads, 0, st>>>(x, segs, stride, parts);
-  finalize_kernel<<<1, 1024, 0, st>>>(parts, grid, 0, book, result, nullptr, nullptr);
+  const int cap = stats_grid_cap();
+  const int64_t grid = sampled < cap ? sampled : cap;
+  unsigned* done = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(parts) - 64);
+  cudaError_t e = cudaMemsetAsync(done, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(x, segs, stride, parts, done, 0,
+                                                                    book, result);
   return cudaGetLastError();
 }
 
@@ -230,7 +322,7 @@ cudaError_t launch_codebook_sampled(const uint16_t* x, const StatSegs& segs, int
 cudaError_t launch_finalize(const Partial* parts, int64_t nparts, int64_t total, uint8_t* book,
                             double* result, const uint8_t* guess, int* mismatch,
                             cudaStream_t st) {
-  finalize_kernel<<<1, 1024, 0, st>>>(parts, nparts, total, book, result, guess, mismatch);
+  finalize_kernel<<<1, kThreads, 0, st>>>(parts, nparts, total, book, result, guess, mismatch);
   return cudaGetLastError();
 }
 

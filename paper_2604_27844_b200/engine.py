@@ -27,9 +27,22 @@ def words_view(t: torch.Tensor) -> torch.Tensor:
     return t.contiguous().view(-1)
 
 
-def workspace(total_elems: int, nseg: int, device) -> torch.Tensor:
+_WS: dict = {}
+
+
+def workspace(total_elems: int, nseg: int, device, stream=None) -> torch.Tensor:
+    """Scratch for one call.  Cached per (device, stream) and grown on demand,
+    so steady-state calls (and CUDA-graph captures) allocate nothing; calls on
+    one stream are ordered, so reuse is safe."""
     nbytes = int(lib().zc_workspace_bytes(int(total_elems), int(nseg)))
-    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+    dev = torch.device(device)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev.index, int(s.cuda_stream))
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+        _WS[key] = buf
+    return buf
 
 
 @functools.lru_cache(maxsize=1024)
@@ -55,7 +68,7 @@ def measured_codebook(words: torch.Tensor, segs=None, stream=None):
     book = torch.empty(8, dtype=torch.uint8, device=dev)
     result = torch.empty(3, dtype=torch.float64, device=dev)
     total = sum(n for _, n in segs)
-    ws = workspace(total, len(segs), dev)
+    ws = workspace(total, len(segs), dev, stream)
     st = check(lib().zc_codebook_measured(
         words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
         i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
@@ -71,7 +84,7 @@ def modal_codebook(words: torch.Tensor, segs=None, stream=None) -> torch.Tensor:
     dev = words.device
     book = torch.empty(8, dtype=torch.uint8, device=dev)
     total = sum(n for _, n in segs)
-    ws = workspace(total, len(segs), dev)
+    ws = workspace(total, len(segs), dev, stream)
     check(lib().zc_codebook_modal(
         words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
         i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
@@ -99,7 +112,7 @@ def encode(words: torch.Tensor, segs, book: torch.Tensor, gs_log2: int,
     if frame_len is None:
         frame_len = torch.empty(nseg, dtype=torch.int64, device=words.device)
     total = sum(n for _, n in segs)
-    ws = workspace(total, nseg, words.device)
+    ws = workspace(total, nseg, words.device, stream)
     for lo in range(0, nseg, _lib.MAX_SEGMENTS):
         part = segs[lo:lo + _lib.MAX_SEGMENTS]
         offs = list(frame_offs)[lo:lo + _lib.MAX_SEGMENTS]
@@ -126,7 +139,7 @@ def encode_measured(words: torch.Tensor, segs, gs_log2: int, frames: torch.Tenso
     book = torch.empty(8, dtype=torch.uint8, device=dev)
     result = torch.empty(3, dtype=torch.float64, device=dev)
     total = sum(n for _, n in segs)
-    ws = workspace(total, nseg, dev)
+    ws = workspace(total, nseg, dev, stream)
     check(lib().zc_encode_measured(
         words.data_ptr(), i64s(o for o, _ in segs), i64s(n for _, n in segs), i64s(frame_offs),
         nseg, int(gs_log2), frames.data_ptr(), ws.data_ptr(), ws.numel(), frame_len.data_ptr(),
@@ -151,7 +164,7 @@ def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_
     if err is None:
         err = torch.empty(nseg, dtype=torch.int32, device=dev)
     total = sum(int(c) for c in counts)
-    ws = workspace(total, nseg, dev)
+    ws = workspace(total, nseg, dev, stream)
     for lo in range(0, nseg, _lib.MAX_SEGMENTS):
         hi = lo + _lib.MAX_SEGMENTS
         check(lib().zc_decode(

@@ -61,9 +61,20 @@ def main():
         c2 = int(e2.item())
         assert c2 == engine.ERR_OK, engine.err_message(c2)
         assert torch.equal(frames[:F], ref) and torch.equal(out, w)
-    t_stats = timed(lambda: engine.measured_codebook(w))
-    t_enc = timed(lambda: engine.encode(w, [(0, n)], book, 9, frames, [0], flen))
-    t_dec = timed(lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0]))
+    def graphed(fn):
+        # CUDA-graph replay: measures device time without host launch overhead
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g.replay
+    t_stats = timed(graphed(lambda: engine.measured_codebook(w)))
+    t_enc = timed(graphed(lambda: engine.encode(w, [(0, n)], book, 9, frames, [0], flen)))
+    t_dec = timed(graphed(lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0])))
+    t_step = timed(graphed(lambda: (engine.encode_measured(w, [(0, n)], 9, frames, [0], flen),
+                                    engine.decode([frames.data_ptr()], [0], None, [n], out,
+                                                  [0]))))
     copy_dst = torch.empty_like(w)
     t_copy = timed(lambda: copy_dst.copy_(w))
     r = dict(n=n, frame=F, ratio=2 * n / F,
@@ -71,6 +82,7 @@ def main():
              encode_ms=t_enc, encode_GBps=(2 * n + F) / t_enc / 1e6,
              decode_ms=t_dec, decode_GBps=(2 * n + F) / t_dec / 1e6,
              copy_ms=t_copy, copy_GBps=4 * n / t_copy / 1e6,
+             step_ms=t_step, step_GBps=2 * n / t_step / 1e6,
              sigma=float(res[0].item()), book=book[:7].tolist())
     print(json.dumps(r))
 

@@ -237,3 +237,19 @@ def test_all_gather_p2p_pull_decode(world):
     for outs in run_ranks(world, body):
         for z, r in outs:
             assert np.array_equal(z, r)
+
+
+@pytest.mark.parametrize("sizer", [lambda s, d: 4096 * 3 + 17, lambda s, d: (s + d) * 97 + 5,
+                                   lambda s, d: 0 if d == 1 else 5000 + s])
+def test_all_to_all_p2p_pull_decode(sizer):
+    from paper_2604_27844_b200.collectives import zip_all_to_all_p2p
+
+    def body(comm):
+        ok = True
+        for it in range(3):
+            spec = _a2a_spec(comm, sizer, seed=it)
+            z = zip_all_to_all_p2p(comm, spec)
+            r = reference_all_to_all(comm, spec)
+            ok &= all(np.array_equal(H(a), H(b)) for a, b in zip(z, r))
+        return ok
+    assert all(run_ranks(4, body))

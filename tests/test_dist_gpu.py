@@ -73,6 +73,15 @@ def _p2p_worker(rank, world, port, q):
             local = rank_words(rank + 7 * it, 500_009, sigma=0.02)
             ok &= np.array_equal(H(zip_all_gather(comm, local)),
                                  H(reference_all_gather(comm, local)))
+        from paper_2604_27844_b200.collectives import (AlltoAllSpec, reference_all_to_all,
+                                                       zip_all_to_all_d2)
+        sizes = lambda s, d: (s + d) * 40_961 + 3  # noqa: E731
+        for it in range(2):
+            spec = AlltoAllSpec([rank_words(rank * 31 + q + it, sizes(rank, q))
+                                 for q in range(world)], [sizes(p, rank) for p in range(world)])
+            got = zip_all_to_all_d2(comm, spec)          # routed to the p2p path
+            ref = reference_all_to_all(comm, spec)
+            ok &= all(np.array_equal(H(a), H(b)) for a, b in zip(got, ref))
         comm.barrier()
         q.put((rank, bool(ok), None))
         dist.destroy_process_group()
