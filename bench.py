@@ -139,6 +139,24 @@ def _agreed_steps(seconds, step, world, dev):
     return int(k.item())
 
 
+def _preflight_p2p(comm, coll, dev) -> bool:
+    """Run one small pull-decode all-gather and check it against the plain
+    collective; any failure on any rank falls back to the NCCL data plane."""
+    import torch
+    import torch.distributed as dist
+    ok = 1
+    try:
+        g = torch.Generator(device=dev).manual_seed(1234 + comm.rank)
+        x = (torch.randn(1 << 20, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+        ok = int(torch.equal(coll.zip_all_gather_p2p(comm, x), coll.reference_all_gather(comm, x)))
+    except Exception as exc:  # noqa: BLE001 - any failure selects the fallback
+        print(f"[rank {comm.rank}] p2p preflight failed: {exc!r}", file=sys.stderr)
+        ok = 0
+    t = torch.tensor([ok], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -282,6 +300,8 @@ def run_ours(args):
     else:
         comm = coll.Communicator.from_process_group()
         comm.use_p2p = args.transport == "p2p"
+        if comm.use_p2p:
+            comm.use_p2p = _preflight_p2p(comm, coll, dev)
 
         def step(rec=False):
             return coll.zip_all_gather(comm, shard)
@@ -346,7 +366,8 @@ def run_ours(args):
         dist.all_reduce(rt, op=dist.ReduceOp.MAX)
         raw_ms = float(rt.item())
         raw = {"value": total_bytes / (raw_ms / 1e3) / 1e9, "ms_per_step": raw_ms,
-               "backend": args.backend, "transport": args.transport,
+               "backend": args.backend,
+               "transport": "p2p" if getattr(comm, "use_p2p", False) else "nccl",
                "speedup_zip_over_raw": raw_ms / ms}
 
     # ---- roofline of the dominant kernel (decode) ---------------------------
@@ -424,6 +445,138 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _gpu_mix(kind: str, n: int, dev):
+    """C4 gradient mixes (SURVEY Appendix C.4 recipe) generated on the GPU."""
+    import torch
+    g = torch.Generator(device=dev).manual_seed(1)
+    sign = torch.where(torch.rand(n, device=dev, generator=g) < 0.5, -1.0, 1.0)
+    if kind == "lognormal2":
+        v = torch.exp(torch.randn(n, device=dev, generator=g) * 2.0 - 8.0) * sign
+        return v.to(torch.bfloat16)
+    gauss = torch.randn(n, device=dev, generator=g) * 1e-3
+    ln = torch.exp(torch.randn(n, device=dev, generator=g) - 8.0) * sign
+    v = torch.where(torch.rand(n, device=dev, generator=g) < 0.5, gauss, ln)
+    if kind == "mix_x1000":
+        idx = torch.randint(0, n, (n // 1000,), device=dev, generator=g)
+        v[idx] *= 1000.0
+    elif kind == "mix_n10":
+        idx = torch.randint(0, n, (n // 10000,), device=dev, generator=g)
+        v[idx] = torch.randn(idx.numel(), device=dev, generator=g) * 10.0
+    return v.to(torch.bfloat16)
+
+
+def run_grad_mix(args):
+    """BASELINE configs[3]: codec throughput and ratio on gradient mixes, 1 GPU."""
+    import torch
+    from paper_2604_27844_b200 import engine
+    dev = torch.device("cuda", 0)
+    n = 1 << 28
+    for kind in ("mix", "mix_x1000", "mix_n10", "lognormal2"):
+        w = engine.words_view(_gpu_mix(kind, n, dev))
+        frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device=dev)
+        out = torch.empty_like(w)
+        flen = torch.empty(1, dtype=torch.int64, device=dev)
+        err = torch.empty(1, dtype=torch.int32, device=dev)
+        enc = lambda: engine.encode_measured(w, [(0, n)], 9, frames, [0], flen)  # noqa: E731
+        dec = lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err)  # noqa: E731
+        enc()
+        dec()
+        torch.cuda.synchronize()
+        assert int(err.item()) == engine.ERR_OK and torch.equal(out, w)
+        F = int(flen.item())
+        ge, gd = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ge):
+            enc()
+        with torch.cuda.graph(gd):
+            dec()
+        times = {}
+        for name, g in (("encode", ge), ("decode", gd)):
+            for _ in range(args.warmup):
+                g.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            for _ in range(args.steps):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            times[name] = a.elapsed_time(b) / args.steps
+        print(json.dumps({
+            "metric": METRIC, "workload": f"c4 gradient {kind}", "n": n,
+            "ratio": 2 * n / F, "escape_rate": None,
+            "codebook_encode_GBps": 2 * n / (times["encode"] / 1e3) / 1e9,
+            "decode_GBps": 2 * n / (times["decode"] / 1e3) / 1e9,
+            "encode_ms": times["encode"], "decode_ms": times["decode"],
+            "note": "GB/s of uncompressed BF16; ratio < 1 means the frame expands "
+                    "(the switcher then picks the raw collective)"}), flush=True)
+
+
+def run_moe_a2a(args):
+    """BASELINE configs[2]: MoE dispatch + combine all-to-all, hidden 4096,
+    top-k 8, T tokens per rank, uniform routing; compressed vs plain."""
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    if args.share_gpu:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(args.backend)
+    from paper_2604_27844_b200 import collectives as coll
+    comm = coll.Communicator.from_process_group()
+    comm.use_p2p = args.transport == "p2p" and _preflight_p2p(comm, coll, dev)
+    hidden, topk, T = 4096, 8, args.tokens
+    rows = T * topk
+    per = rows // world
+    g = torch.Generator(device=dev).manual_seed(rank)
+    x = torch.randn(rows * hidden, device=dev, generator=g).to(torch.bfloat16)
+    chunks = [x[q * per * hidden:(q + 1) * per * hidden] for q in range(world)]
+    spec = coll.AlltoAllSpec(chunks, [per * hidden] * world)
+
+    def zip_step():
+        got = coll.zip_all_to_all_d2(comm, spec)                    # dispatch
+        back = coll.AlltoAllSpec(got, [per * hidden] * world)
+        return coll.zip_all_to_all_d2(comm, back)                   # combine
+
+    def raw_step():
+        got = coll.reference_all_to_all(comm, spec)
+        return coll.reference_all_to_all(comm, coll.AlltoAllSpec(got, [per * hidden] * world))
+
+    res = zip_step()
+    ok = all(torch.equal(a.view(torch.int16), b.view(torch.int16))
+             for a, b in zip(res, [c.view(torch.int16) for c in chunks]))
+    assert ok, "combine(dispatch(x)) != x"
+    ms = {}
+    for name, fn in (("zip", zip_step), ("raw", raw_step)):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms[name] = float(t.item())
+    send_bytes = 2 * rows * hidden * 2                             # dispatch + combine, per rank
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "workload": "c3 qwen3-moe dispatch+combine all-to-all",
+            "n_gpus": world, "tokens_per_rank": T, "topk": topk, "hidden": hidden,
+            "value": world * send_bytes / (ms["zip"] / 1e3) / 1e9, "unit": "GB/s",
+            "ms_per_step": ms["zip"], "raw_ms_per_step": ms["raw"],
+            "raw_value": world * send_bytes / (ms["raw"] / 1e3) / 1e9,
+            "speedup_zip_over_raw": ms["raw"] / ms["zip"],
+            "transport": "p2p" if comm.use_p2p else "nccl", "backend": args.backend}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -434,8 +587,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-settle", type=float, default=1.0)
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly (no CUDA graph)")
+    ap.add_argument("--workload", default="layer_ag", choices=["layer_ag", "moe_a2a", "grad_mix"],
+                    help="layer_ag: the headline line (configs[1]); moe_a2a: configs[2]; "
+                         "grad_mix: configs[3]")
+    ap.add_argument("--tokens", type=int, default=4096, help="moe_a2a tokens per rank")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
                     help="nccl: frames move with NCCL collectives, decode after arrival; "
                          "p2p: decoder pulls peer frames over NVLink (IPC symmetric buffers)")
     ap.add_argument("--share-gpu", action="store_true",
@@ -445,6 +602,10 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "grad_mix":
+        run_grad_mix(args)
+    elif args.workload == "moe_a2a":
+        run_moe_a2a(args)
     else:
         run_ours(args)
 
