@@ -27,10 +27,10 @@ def launches(tag):
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 items.append((d["Kernel Name"], float(d["Metric Value"])))
     zc = [(k, v) for k, v in items if k.startswith("zc::")]
-    # one bench step = stats, finalize, encode pass 1, fix-up, decode; take the last step
+    # one bench step = stats (+finalize), encode (+fix-up), decode; take the last step
     names = ["stats_kernel", "finalize_kernel", "encode_tiles_kernel", "encode_fixup_kernel",
              "decode_ring_kernel"]
-    step = zc[-5:]
+    step = zc[-3:]
     total = sum(v for _, v in step)
     lines = [f"# launch list, one bench step (ncu gpu__time_duration, cold-cache, serialised)",
              f"# source: gpurun_out/launches_bench_{tag}.csv ({len(items)} launches)"]
