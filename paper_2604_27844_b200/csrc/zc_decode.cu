@@ -475,6 +475,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
           if (b_gi) tma_load_1d(S.gi, gsrc, b_gi, full + st);
           if (eb) tma_load_1d(S.esc, eal, (uint32_t)eb, full + st);
         }
+        __syncwarp();   // reconverge before the next shuffle (no BRA.DIV slow path)
       }
     }
     return;
@@ -501,9 +502,26 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
   for (int k = 0; k < nfast; ++k) {
     // ---------------- lean path: gs = 512, all 16 elements valid -----------
     const int st = k & (kDStages - 1);
-    mbar_wait(full + st, (uint32_t)((k / kDStages) & 1));
+    mbar_wait_warp(full + st, (uint32_t)((k / kDStages) & 1));
     const DStage& S = ring[st];
     const uint4 sv = *reinterpret_cast<const uint4*>(S.sm + ct * kEPT);
+#ifdef ZC_EXP_RING_ONLY
+    {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+      uint16_t* dst = out_seg + ((t_begin + k) * kTile + ct * kEPT);
+#if defined(ZC_EXP_NOSTORE)
+      if (sv.x == 0x9E3779B9u && sv.y == 0x7F4A7C15u) *dst = 1;
+#elif defined(ZC_EXP_PLAINSTORE)
+      *reinterpret_cast<uint4*>(dst) = sv;
+      *reinterpret_cast<uint4*>(dst + 8) = sv;
+#else
+      st_stream_v4(dst, sv);
+      st_stream_v4(dst + 8, sv);
+#endif
+      continue;
+    }
+#endif
     const uint32_t p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + ct * 2);
     const uint32_t p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + ct * 2);
     const uint32_t p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
@@ -572,7 +590,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     // ---------------- general path ---------------------------------------
     const int64_t k = t - t_begin;
     const int st = (int)(k % kDStages);
-    mbar_wait(full + st, (uint32_t)((k / kDStages) & 1));
+    mbar_wait_warp(full + st, (uint32_t)((k / kDStages) & 1));
     const DStage& S = ring[st];
     const int64_t tile_base = t * kTile;
     const int64_t base = tile_base + (int64_t)ct * kEPT;

@@ -376,7 +376,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     for (int k = 0; k < nfast; ++k) {
       const int st = k & (kStages - 1);
       const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
-      mbar_wait(bars + st, (uint32_t)((k / kStages) & 1));
+      mbar_wait_warp(bars + st, (uint32_t)((k / kStages) & 1));
       const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
       const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
       const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
@@ -468,7 +468,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     const int64_t tile_valid = n - t * kTile;
     const int tma_elems = aligned ? (int)((((tile_valid >= kTile ? kTile : tile_valid) * 2) & ~15) / 2) : 0;
 
-    mbar_wait(bars + st, (uint32_t)((k / kStages) & 1));
+    mbar_wait_warp(bars + st, (uint32_t)((k / kStages) & 1));
 
     uint32_t w[8];
     const bool from_smem = full && tid * kEPT + kEPT <= tma_elems;

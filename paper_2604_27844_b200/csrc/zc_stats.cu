@@ -87,7 +87,7 @@ stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t stride
     const int64_t tvalid = segs.n[sg] - base;
     const int tma_elems = ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)
         ? (int)((((tvalid >= kTile ? kTile : tvalid) * 2) & ~15) / 2) : 0;
-    mbar_wait(bars + st, (uint32_t)((k / kSStages) & 1));
+    mbar_wait_warp(bars + st, (uint32_t)((k / kSStages) & 1));
     const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kSStageBytes);
     uint32_t w[8];
     uint32_t valid = 0xFFFFu;
