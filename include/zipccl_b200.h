@@ -56,10 +56,17 @@ int64_t zc_workspace_bytes(int64_t total_elems, int nseg);
  * the all-to-all scope of collectives._prepare_frames (collectives.py:230-242).
  * Writes book_dev[0..6] = entries, book_dev[7] = 0 and
  * result_dev[0] = sigma (NaN if no finite element), result_dev[1] = finite
- * count, result_dev[2] = 1 (analytic) / 2 (modal fallback). */
+ * count, result_dev[2] = 1 (analytic) / 2 (modal fallback) / 3 (analytic,
+ * certified).  Without ZC_SIGMA_EXACT in `flags` a packed-fp32 pass with a
+ * rigorous error bound decides the codebook whenever the whole sigma
+ * interval maps to one codebook (path 3, result_dev[0] then within ~2e-6
+ * relative of the f64 statistic); otherwise, and always with
+ * ZC_SIGMA_EXACT, the f64 pass runs (paths 1/2).  The codebook is the
+ * reference's either way. */
+#define ZC_SIGMA_EXACT 1
 int zc_codebook_measured(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
                          int nseg, void* ws, int64_t ws_bytes, uint8_t* book_dev,
-                         double* result_dev, void* stream);
+                         double* result_dev, int flags, void* stream);
 
 /* Replaces the modal fallback of codec.codebook_for for an explicit sigma that
  * is 0, negative or non-finite (codec.py:179-185): window around the first

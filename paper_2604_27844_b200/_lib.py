@@ -36,7 +36,8 @@ EXPORTS = {
     "zc_static_bytes": (_i64, [_i64, _int]),
     "zc_max_frame_bytes": (_i64, [_i64, _int]),
     "zc_workspace_bytes": (_i64, [_i64, _int]),
-    "zc_codebook_measured": (_int, [_vp, _P(_i64), _P(_i64), _int, _vp, _i64, _vp, _vp, _vp]),
+    "zc_codebook_measured": (_int, [_vp, _P(_i64), _P(_i64), _int, _vp, _i64, _vp, _vp, _int,
+                                    _vp]),
     "zc_codebook_modal": (_int, [_vp, _P(_i64), _P(_i64), _int, _vp, _i64, _vp, _vp]),
     "zc_encode": (_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _int, _vp, _int, _vp, _vp, _i64,
                          _vp, _vp]),
@@ -53,6 +54,9 @@ EXPORTS = {
     "zc_signal_peers": (_int, [_P(_vp), _int, _int, ctypes.c_uint64, _vp]),
     "zc_wait_signals": (_int, [_vp, _int, _int, ctypes.c_uint64, ctypes.c_int64, _vp, _vp]),
 }
+
+
+ABI_VERSION = 2   # zc_abi_version() of the matching include/zipccl_b200.h
 
 
 def lib():
@@ -74,6 +78,10 @@ def lib():
                 continue
             fn.restype = res
             fn.argtypes = args
+        if handle.zc_abi_version() != ABI_VERSION:
+            raise ExtensionMissingError(
+                f"{LIB_PATH} has ABI {handle.zc_abi_version()}, expected {ABI_VERSION}; "
+                "rebuild with `python -m paper_2604_27844_b200.build`")
         _lib = handle
         return _lib
 

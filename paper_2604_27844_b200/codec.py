@@ -185,7 +185,7 @@ def measure_sigma(data) -> float:
     words = device_words(data)
     if words.numel() == 0:
         raise DegenerateDataError("measure_sigma: empty buffer")
-    _, result = engine.measured_codebook(words)
+    _, result = engine.measured_codebook(words, exact=True)
     sigma, count, _ = result.cpu().tolist()
     if count == 0:
         raise DegenerateDataError("measure_sigma: no finite elements")

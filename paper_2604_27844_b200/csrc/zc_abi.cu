@@ -6,7 +6,7 @@
 
 namespace zc {
 cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
-                                     double*, cudaStream_t);
+                                     double*, int, cudaStream_t);
 cudaError_t launch_codebook_modal(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
                                   cudaStream_t);
 cudaError_t launch_encode(const uint16_t*, const EncodeSegs&, const uint8_t*, uint8_t*, void*,
@@ -31,7 +31,7 @@ int status_of(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
 
 extern "C" {
 
-int zc_abi_version(void) { return 1; }
+int zc_abi_version(void) { return 2; }
 
 int zc_tile_elements(void) { return kTile; }
 
@@ -67,7 +67,7 @@ int64_t zc_workspace_bytes(int64_t total_elems, int nseg) {
 
 int zc_codebook_measured(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n, int nseg,
                          void* ws, int64_t ws_bytes, uint8_t* book_dev, double* result_dev,
-                         cudaStream_t stream) {
+                         int flags, cudaStream_t stream) {
   if (nseg < 0 || nseg > kMaxSegments || !book_dev || !result_dev || !ws) return kStatusBadArg;
   StatSegs s{};
   int k = 0;
@@ -85,7 +85,8 @@ int zc_codebook_measured(const uint16_t* x, const int64_t* seg_off, const int64_
   s.nseg = k;
   if (k > 0 && !x) return kStatusBadArg;
   if (128 + 32 * s.tile_start[k] > ws_bytes) return kStatusWorkspace;
-  return status_of(launch_codebook_measured(x, s, total, ws, book_dev, result_dev, stream));
+  return status_of(launch_codebook_measured(x, s, total, ws, book_dev, result_dev, flags & 1,
+                                            stream));
 }
 
 int zc_codebook_modal(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n, int nseg,

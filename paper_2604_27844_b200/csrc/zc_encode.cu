@@ -720,7 +720,7 @@ cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8
 }
 
 cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
-                                     double*, cudaStream_t);
+                                     double*, int, cudaStream_t);
 cudaError_t launch_codebook_sampled(const uint16_t*, const StatSegs&, int64_t, Partial*,
                                     uint8_t*, double*, cudaStream_t);
 cudaError_t launch_finalize(const Partial*, int64_t, int64_t, uint8_t*, double*, const uint8_t*,
@@ -744,7 +744,7 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   const int64_t ntiles = segs.tile_start[segs.nseg];
   uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
   if (!speculative || ntiles < kSpecMinTiles) {
-    cudaError_t e = launch_codebook_measured(x, ss, total, ws, book, result, st);
+    cudaError_t e = launch_codebook_measured(x, ss, total, ws, book, result, 0, st);
     if (e != cudaSuccess) return e;
     return launch_encode(x, segs, book, frames, ws, frame_len, st);
   }

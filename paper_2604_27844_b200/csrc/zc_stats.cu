@@ -59,7 +59,10 @@ __device__ __forceinline__ void stats_issue(const uint16_t* x, const StatSegs& s
 __global__ void __launch_bounds__(kThreads)
 stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t stride,
              Partial* __restrict__ out, unsigned* __restrict__ done, int64_t total_words,
-             uint8_t* __restrict__ book, double* __restrict__ result) {
+             uint8_t* __restrict__ book, double* __restrict__ result,
+             const int* __restrict__ need) {
+  // fallback launch behind the certified pass: nothing to do when it decided
+  if (need != nullptr && *need == 0) return;
   extern __shared__ __align__(128) uint8_t s_dyn[];
   uint8_t* ring = s_dyn;
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kSStages * kSStageBytes);
@@ -158,6 +161,16 @@ __device__ double window_coverage(double sigma, double x) {
 
 __device__ int clamp_base(int b) { return b < -126 ? -126 : (b > 121 ? 121 : b); }
 
+// derive_codebook (codec.py:149-161): floor/ceil of log2(sigma) + offset,
+// larger coverage wins, tie to floor; clamped like write_window
+__device__ int derive_base(double sigma) {
+  const double xo = log2(sigma) + kBaseExponentOffset;
+  const double lo = floor(xo), hi = ceil(xo);
+  const int base = (lo == hi || window_coverage(sigma, lo) >= window_coverage(sigma, hi))
+                       ? (int)lo : (int)hi;
+  return clamp_base(base);
+}
+
 __device__ void write_window(uint8_t* book, int base) {
   const int first = clamp_base(base) + 127;
   for (int i = 0; i < 7; ++i) book[i] = (uint8_t)(first + i);
@@ -212,12 +225,7 @@ __device__ void finalize_block(const Partial* parts, int64_t nparts, int64_t tot
     result[0] = sigma;
     result[1] = cn;
     if (cn > 0.0 && isfinite(sigma) && sigma > 0.0) {
-      // derive_codebook (codec.py:149-161)
-      const double xo = log2(sigma) + kBaseExponentOffset;
-      const double lo = floor(xo), hi = ceil(xo);
-      const int base = (lo == hi || window_coverage(sigma, lo) >= window_coverage(sigma, hi))
-                           ? (int)lo : (int)hi;
-      write_window(book, base);
+      write_window(book, derive_base(sigma));
       result[2] = 1.0;
     } else {
       // modal fallback (codec.py:181-185): with sigma 0 or no finite value the
@@ -244,6 +252,196 @@ finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total
                 uint8_t* __restrict__ book, double* __restrict__ result,
                 const uint8_t* __restrict__ guess, int* __restrict__ mismatch) {
   finalize_block(parts, nparts, total_words, book, result, guess, mismatch);
+}
+
+// ---- certified fast statistic ------------------------------------------------
+// Every element contributes d = x - K (K = the first element when finite, else
+// 0; the same K everywhere, so partials merge by plain addition) to per-tile
+// sums kept in packed fp32 (FADD2/FFMA2, 8 terms per lane), flushed to f64
+// once per tile.  A non-finite element poisons the sums (inf/NaN propagate),
+// which routes the call to the exact f64 kernel.  Error bound (u = 2^-24):
+// per element fl(x - K) = d(1+δ), |δ| <= u; 8-term fp32 chains add <= γ_8;
+// f64 accumulation adds <= 2^-36 relative; with Q = Σd² (>= 0) and
+// |S1| <= sqrt(N Q):  |ΔS2| <= 11u·Q, |ΔS1| <= 10u·Σ|d|, so
+//   |ΔM2| = |ΔS2 - (2 S1 ΔS1 + ΔS1²)/N| <= 32u·Q + 2^-34·Q + N·2^-150
+// (the last term: fp32 underflow of d²).  The codebook is certified when
+// derive_base() agrees at both ends of sigma = sqrt((M2 ± Δ)/N), widened by
+// 2^-40 for the reference's own f64 evaluation (np.std two-pass error); the
+// reference's sigma lies in that interval and derive_base is monotone, so
+// its codebook is this one.  Otherwise *need = 1 and the exact pass runs.
+struct SumPartial {
+  double s1, s2;
+};
+
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ double f2_sum(uint64_t v) {
+  return (double)__uint_as_float((uint32_t)v) + (double)__uint_as_float((uint32_t)(v >> 32));
+}
+
+__device__ void certify_block(const SumPartial* parts, int64_t nparts, int64_t total,
+                              uint8_t* book, double* result, int* need) {
+  __shared__ double c_1[kWarps], c_2[kWarps];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t per = (nparts + kThreads - 1) / kThreads;
+  double a1 = 0.0, a2 = 0.0;
+  for (int64_t i = t * per; i < (t + 1) * per && i < nparts; ++i) {
+    a1 += __ldcg(&parts[i].s1);
+    a2 += __ldcg(&parts[i].s2);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {   // fixed tree: lane i absorbs lane i+o
+    const double b1 = __shfl_down_sync(0xffffffffu, a1, o);
+    const double b2 = __shfl_down_sync(0xffffffffu, a2, o);
+    if ((lane & (2 * o - 1)) == 0) { a1 += b1; a2 += b2; }
+  }
+  if (lane == 0) { c_1[warp] = a1; c_2[warp] = a2; }
+  __syncthreads();
+  if (t != 0) return;
+  double S1 = 0.0, S2 = 0.0;
+  for (int i = 0; i < kWarps; ++i) { S1 += c_1[i]; S2 += c_2[i]; }
+  const double N = (double)total;
+  int decided = 0;
+  if (total > 0 && isfinite(S1) && isfinite(S2)) {
+    const double m2 = S2 - S1 * (S1 / N);
+    const double q = S2 * (1.0 + 0x1p-20);                 // >= true Q
+    const double delta = (32.0 * 0x1p-24 + 0x1p-34) * q + N * 0x1p-150;
+    if (m2 - delta > 0.0) {
+      const double s_lo = sqrt((m2 - delta) / N) * (1.0 - 0x1p-40);
+      const double s_hi = sqrt((m2 + delta) / N) * (1.0 + 0x1p-40);
+      if (isfinite(s_hi)) {
+        const int b = derive_base(s_lo);
+        if (b == derive_base(s_hi)) {
+          write_window(book, b);
+          result[0] = sqrt(m2 / N);
+          result[1] = N;
+          result[2] = 3.0;                                   // analytic, certified
+          decided = 1;
+        }
+      }
+    }
+  }
+  *need = decided ? 0 : 1;
+}
+
+__global__ void __launch_bounds__(kThreads)
+sums_kernel(const uint16_t* __restrict__ x, const StatSegs segs, SumPartial* __restrict__ out,
+            unsigned* __restrict__ done, int64_t total, uint8_t* __restrict__ book,
+            double* __restrict__ result, int* __restrict__ need) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  uint8_t* ring = s_dyn;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kSStages * kSStageBytes);
+  const int tid = threadIdx.x;
+  const int64_t ntiles = segs.tile_start[segs.nseg];
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = blockIdx.x * per;
+  const int64_t i1 = (i0 + per < ntiles) ? i0 + per : ntiles;
+  if (tid == 0) {
+    for (int k = 0; k < kSStages; ++k) mbar_init(bars + k, 1);
+    fence_mbar_init();
+    for (int k = 0; k < kSStages && i0 + k < i1; ++k)
+      stats_issue(x, segs, i0 + k, ring + k * kSStageBytes, bars + k);
+  }
+  // shift: the first element when finite (its word also pads partial tiles)
+  uint32_t kw = x[segs.x_off[0]];
+  if ((kw & 0x7F80u) == 0x7F80u) kw = 0;
+  const uint32_t kpair = kw | (kw << 16);
+  const uint64_t K2 = (uint64_t)(kpair & 0xFFFF0000u) << 32 | (uint64_t)(kpair << 16);
+  __syncthreads();
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t i = i0; i < i1; ++i) {
+    const int k = (int)(i - i0);
+    const int st = k & (kSStages - 1);
+    mbar_wait_warp(bars + st, (uint32_t)((k / kSStages) & 1));
+    const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kSStageBytes);
+    uint32_t w[8];
+    const int sg = find_seg(segs.tile_start, segs.nseg, i);
+    const uint16_t* xs = x + segs.x_off[sg];
+    const int64_t base = (i - segs.tile_start[sg]) * kTile;
+    const int64_t tvalid = segs.n[sg] - base;
+    const int tma_elems = ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)
+        ? (int)((((tvalid >= kTile ? kTile : tvalid) * 2) & ~15) / 2) : 0;
+    if (tid * kEPT + kEPT <= tma_elems) {
+      const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
+      const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else {
+      const int64_t nvalid = tvalid - (int64_t)tid * kEPT;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e0 = tid * kEPT + 2 * j;
+        uint32_t lo = kw, hi = kw;                       // d = 0 outside the segment
+        if (2 * j < nvalid) lo = (e0 < tma_elems) ? tw[e0] : xs[base + e0];
+        if (2 * j + 1 < nvalid) hi = (e0 + 1 < tma_elems) ? tw[e0 + 1] : xs[base + e0 + 1];
+        w[j] = lo | (hi << 16);
+      }
+    }
+    uint64_t a1 = 0, a2 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t v = (uint64_t)(w[j] & 0xFFFF0000u) << 32 | (uint64_t)(w[j] << 16);
+      const uint64_t d = f2_sub(v, K2);
+      a1 = f2_add(a1, d);
+      a2 = f2_fma(d, d, a2);
+    }
+    s1 += f2_sum(a1);
+    s2 += f2_sum(a2);
+    __syncthreads();                                   // stage free
+    if (tid == 0 && i + kSStages < i1) {
+      fence_proxy_async();
+      stats_issue(x, segs, i + kSStages, ring + st * kSStageBytes, bars + st);
+    }
+  }
+  // fixed-order CTA sum
+  __shared__ double b_1[kWarps], b_2[kWarps];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_down_sync(0xffffffffu, s1, o);
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  }
+  if ((tid & 31) == 0) { b_1[tid >> 5] = s1; b_2[tid >> 5] = s2; }
+  __syncthreads();
+  __shared__ bool s_last;
+  if (tid == 0) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int i = 0; i < kWarps; ++i) { t1 += b_1[i]; t2 += b_2[i]; }
+    out[blockIdx.x] = SumPartial{t1, t2};
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    certify_block(out, gridDim.x, total, book, result, need);
+  }
+}
+
+static int sums_grid_cap() {
+  static int cap = 0;
+  if (cap == 0) {
+    cudaFuncSetAttribute(sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stats_dyn_smem());
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sums_kernel, kThreads, stats_dyn_smem());
+    cap = sms * (occ > 0 ? occ : 1);
+  }
+  return cap;
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -273,18 +471,33 @@ __global__ void mode_kernel(const unsigned long long* __restrict__ hist, int64_t
   write_window(book, all_zero ? -6 : mode - 127 - 3);
 }
 
+// Workspace: [64] exact-pass counter, [68] certified-pass counter, [72] need
+// flag, [128..) per-CTA partials (both passes; they run one after the other).
+// exact != 0: result[0] must be the f64 statistic itself (measure_sigma);
+// otherwise the certified pass decides the codebook and the exact kernel
+// returns at once unless the certificate failed.
 cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, int64_t total,
-                                     void* ws, uint8_t* book, double* result, cudaStream_t st) {
+                                     void* ws, uint8_t* book, double* result, int exact,
+                                     cudaStream_t st) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
-  Partial* parts = reinterpret_cast<Partial*>(reinterpret_cast<uint8_t*>(ws) + 128);
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
+  Partial* parts = reinterpret_cast<Partial*>(w8 + 128);
   const int cap = stats_grid_cap();
   const int64_t grid = ntiles < cap ? ntiles : cap;
-  unsigned* done = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(ws) + 64);
+  unsigned* done = reinterpret_cast<unsigned*>(w8 + 64);
+  unsigned* done_sums = reinterpret_cast<unsigned*>(w8 + 68);
+  int* need = reinterpret_cast<int*>(w8 + 72);
   if (grid > 0) {
-    cudaError_t e = cudaMemsetAsync(done, 0, sizeof(unsigned), st);
+    cudaError_t e = cudaMemsetAsync(done, 0, 16, st);
     if (e != cudaSuccess) return e;
-    stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(x, segs, 1, parts, done,
-                                                                      total, book, result);
+    if (!exact) {
+      const int scap = sums_grid_cap();
+      const int64_t sgrid = ntiles < scap ? ntiles : scap;
+      sums_kernel<<<(unsigned)sgrid, kThreads, stats_dyn_smem(), st>>>(
+          x, segs, reinterpret_cast<SumPartial*>(parts), done_sums, total, book, result, need);
+    }
+    stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(
+        x, segs, 1, parts, done, total, book, result, exact ? nullptr : need);
   } else {
     finalize_kernel<<<1, kThreads, 0, st>>>(parts, 0, total, book, result, nullptr, nullptr);
   }
@@ -314,7 +527,7 @@ cudaError_t launch_codebook_sampled(const uint16_t* x, const StatSegs& segs, int
   cudaError_t e = cudaMemsetAsync(done, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
   stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(x, segs, stride, parts, done, 0,
-                                                                    book, result);
+                                                                    book, result, nullptr);
   return cudaGetLastError();
 }
 

@@ -57,10 +57,15 @@ def book_tensor(entries, device) -> torch.Tensor:
     return _book_cached(tuple(int(e) for e in entries), device.index or 0)
 
 
-def measured_codebook(words: torch.Tensor, segs=None, stream=None):
+SIGMA_EXACT = 1   # zc_codebook_measured flag (include/zipccl_b200.h)
+
+
+def measured_codebook(words: torch.Tensor, segs=None, stream=None, exact: bool = False):
     """K1: sigma over the finite elements of the segments + on-device codebook.
 
     Returns (book uint8[8], result float64[3] = sigma, finite count, path).
+    Path 3 = codebook certified by the packed-fp32 pass (sigma then within
+    ~2e-6 relative); `exact=True` always runs the f64 statistic.
     """
     if segs is None:
         segs = [(0, words.numel())]
@@ -72,7 +77,8 @@ def measured_codebook(words: torch.Tensor, segs=None, stream=None):
     st = check(lib().zc_codebook_measured(
         words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
         i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
-        result.data_ptr(), stream_ptr(stream)), "zc_codebook_measured")
+        result.data_ptr(), SIGMA_EXACT if exact else 0, stream_ptr(stream)),
+        "zc_codebook_measured")
     del st
     return book, result
 

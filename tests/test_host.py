@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 15
     for name in names:
         assert hasattr(lib, name), name
-    assert lib.zc_abi_version() == 1
+    assert lib.zc_abi_version() == 2
     assert lib.zc_tile_elements() == 4096
 
 

@@ -1,0 +1,140 @@
+"""Certified codebook pass (zc_stats.cu sums_kernel + certify_block) against
+the reference statistic: the packed-fp32 pass may decide the codebook only
+when the whole error interval of sigma maps to one codebook; everything near a
+flip threshold, non-finite or badly conditioned must fall back to the exact
+f64 pass (reference bf16.measure_sigma, bf16.py:88-103, and
+codec.derive_codebook, codec.py:149-161)."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import zc_oracle as zo
+
+pytestmark = pytest.mark.gpu
+
+from paper_2604_27844_b200 import engine  # noqa: E402
+
+PATH_EXACT, PATH_MODAL, PATH_CERTIFIED = 1.0, 2.0, 3.0
+
+
+def _measure(host: np.ndarray):
+    x = torch.from_numpy(host.view(np.int16)).cuda()
+    book, res = engine.measured_codebook(x)
+    exact_book, exact = engine.measured_codebook(x, exact=True)
+    return tuple(book[:7].tolist()), res.cpu().tolist(), tuple(exact_book[:7].tolist()), \
+        exact.cpu().tolist()
+
+
+def _flip_sigma(octave: int) -> float:
+    """sigma where derive() switches from floor to ceil inside an octave
+    (bisection on the oracle's decision)."""
+    lo, hi = 2.0 ** octave, 2.0 ** (octave + 1)
+    b_lo = zo.derive(lo)
+    assert zo.derive(hi) != b_lo
+    for _ in range(200):
+        mid = math.sqrt(lo * hi)
+        if zo.derive(mid) == b_lo:
+            lo = mid
+        else:
+            hi = mid
+    return hi
+
+
+def _three_point(target: float, n: int, rel: float, seed: int) -> np.ndarray:
+    """n words in {+a, -a, 0} (equal +a/-a counts: mean exactly 0) whose
+    population std is target * (1 + rel) to ~3e-7 relative: sigma = a * sqrt(2p / n)."""
+    want = target * (1.0 + rel)
+    e = math.floor(math.log2(want))
+    best = None
+    for m in range(128, 256):                       # bf16 mantissas of one octave
+        for de in (-1, 0):
+            a = m * 2.0 ** (e + de - 7)
+            p = round(want * want * n / (2 * a * a))
+            if not 1 <= p <= n // 2:
+                continue
+            s = a * math.sqrt(2 * p / n)
+            err = abs(s / want - 1.0)
+            if best is None or err < best[0]:
+                best = (err, a, p)
+    _, a, p = best
+    v = np.zeros(n)
+    v[:p], v[p:2 * p] = a, -a
+    np.random.default_rng(seed).shuffle(v)
+    return zo.from_f64(v)
+
+
+def test_certified_on_model_like_data():
+    for seed, s in enumerate([0.02, 1.0, 3e-5, 250.0]):
+        host = zo.gaussian(1 << 20, s, seed=seed)
+        book, res, ebook, eres = _measure(host)
+        assert res[2] == PATH_CERTIFIED, res
+        assert book == ebook == zo.book_for(host)
+        assert res[0] == pytest.approx(eres[0], rel=4e-6)
+        assert res[1] == eres[1] == host.size
+
+
+@pytest.mark.parametrize("octave", [-9, -6, 0, 5])
+@pytest.mark.parametrize("rel", [1e-8, -1e-8, 3e-7, -3e-7])
+def test_near_flip_threshold_falls_back(octave, rel):
+    target = _flip_sigma(octave)
+    host = _three_point(target, 1 << 20, rel, seed=octave & 0xFF)
+    s = zo.sigma(host)
+    assert abs(s / target - 1.0) < 1e-6               # inside the certificate's interval
+    book, res, ebook, _ = _measure(host)
+    assert book == zo.book_for(host) == ebook
+    assert res[2] == PATH_EXACT, res                 # the certificate must refuse
+
+
+def test_far_from_threshold_is_certified():
+    target = _flip_sigma(-6)
+    host = _three_point(target, 1 << 20, 0.05, seed=1)
+    book, res, _, _ = _measure(host)
+    assert res[2] == PATH_CERTIFIED and book == zo.book_for(host)
+
+
+@pytest.mark.parametrize("case", ["first_outlier", "big_mean", "nan", "inf", "neg_inf_pair",
+                                  "constant", "all_nan", "huge"])
+def test_fallback_cases_match_reference(case):
+    n = (1 << 18) + 77
+    host = zo.gaussian(n, 0.02, seed=3)
+    if case == "first_outlier":          # K = x[0] far from the mean: Q >> M2
+        host[0] = zo.from_f64(np.array([1e4]))[0]
+    elif case == "big_mean":             # mean/sigma = 1e4 but K = x[0] near the mean
+        host = zo.from_f64(1000.0 + np.random.default_rng(2).standard_normal(n) * 0.1)
+    elif case == "nan":
+        host[12345] = 0x7FC0
+    elif case == "inf":
+        host[-1] = 0x7F80
+    elif case == "neg_inf_pair":
+        host[5], host[6] = 0x7F80, 0xFF80
+    elif case == "constant":
+        host[:] = 0x3FC0
+    elif case == "all_nan":
+        host[:] = 0x7FC1
+    elif case == "huge":                 # d^2 overflows fp32
+        host[100] = 0x7F00
+    book, res, ebook, eres = _measure(host)
+    assert book == ebook == zo.book_for(host), (case, res)
+    if case in ("nan", "inf", "neg_inf_pair", "constant", "all_nan", "huge"):
+        assert res[2] in (PATH_EXACT, PATH_MODAL), (case, res)
+    # first_outlier: Q/M2 ~ n widens the interval to ~+-25 %, which may still
+    # sit inside one codebook -- certified or not, the book must match
+    if res[2] != PATH_CERTIFIED:
+        assert res == eres or (math.isnan(res[0]) and math.isnan(eres[0]))
+
+
+def test_certified_multi_segment_and_unaligned():
+    rng = np.random.default_rng(9)
+    buf = zo.from_f64(rng.standard_normal(3 * 100_003 + 5) * 0.3)
+    x = torch.from_numpy(buf.view(np.int16)).cuda()
+    segs = [(1, 100_003), (100_004, 0), (200_007, 100_001)]   # odd offsets: no TMA
+    book, res = engine.measured_codebook(x, segs)
+    concat = np.concatenate([buf[o:o + c] for o, c in segs])
+    assert tuple(book[:7].tolist()) == zo.book_for(concat)
+    assert res[1].item() == concat.size
+    assert res[0].item() == pytest.approx(zo.sigma(concat), rel=4e-6)
