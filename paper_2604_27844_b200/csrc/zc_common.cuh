@@ -114,6 +114,27 @@ __device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
   *reinterpret_cast<uint4*>(p) = v;
 }
 
+// Inclusive scan over the first `Lanes` lanes of a warp (all 32 lanes must
+// call it).  shfl.up's lane-valid predicate guards the add: one SHFL + one
+// predicated IADD per step, no lane compare / select.
+template <int Lanes = 32>
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+#pragma unroll
+  for (int o = 1; o < Lanes; o <<= 1)
+    asm volatile("{ .reg .u32 t; .reg .pred p;\n\t"
+                 "shfl.sync.up.b32 t|p, %0, %1, 0, -1;\n\t"
+                 "@p add.u32 %0, %0, t; }"
+                 : "+r"(v) : "r"(o));
+  return v;
+}
+
+// (a & m) | (b & ~m) as one LOP3
+__device__ __forceinline__ uint32_t bitsel(uint32_t m, uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "r"(m), "r"(a), "r"(b));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));

@@ -100,8 +100,8 @@ __device__ __forceinline__ void load_static(const uint8_t* frame, const Layout& 
 // 4 output words from 4 sign-mantissa bytes S and 4 exponent bytes E
 // (codec.py:308-312): lo byte = e0<<7 | s&0x7F, hi byte = s&0x80 | e>>1.
 __device__ __forceinline__ void reassemble4(uint32_t S, uint32_t E, uint32_t& o01, uint32_t& o23) {
-  const uint32_t lo = (S & 0x7F7F7F7Fu) | ((E << 7) & 0x80808080u);
-  const uint32_t hi = (S & 0x80808080u) | ((E >> 1) & 0x7F7F7F7Fu);
+  const uint32_t lo = bitsel(0x80808080u, E << 7, S);
+  const uint32_t hi = bitsel(0x80808080u, S, E >> 1);
   o01 = prmt(lo, hi, 0x5140);
   o23 = prmt(lo, hi, 0x7362);
 }
@@ -195,12 +195,7 @@ decode_lookback_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_
 
     // ---- tile-local scan of escape counts --------------------------------
     const uint32_t cnt = __popc(esc);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
+    uint32_t incl = warp_incl_scan(cnt);
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();                                     // (B)
     uint32_t wbase = 0, agg = 0;
@@ -527,12 +522,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     const uint32_t p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
     const uint32_t esc = ~(p0 | p1 | p2) & 0xFFFFu;
     const uint32_t cnt = __popc(esc);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      incl += (lane >= o) ? v : 0u;
-    }
+    uint32_t incl = warp_incl_scan(cnt);
     const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
     const int gshift = s_gi_shift[st];
     const uint32_t lo32 = (uint32_t)s_lo[st];
@@ -620,12 +610,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     }
     const uint32_t esc = ~(p0 | p1 | p2) & valid16;
     const uint32_t cnt = __popc(esc);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      incl += (lane >= o) ? v : 0u;
-    }
+    uint32_t incl = warp_incl_scan(cnt);
     const uint32_t wexcl = incl - cnt;               // escapes in the warp before me
     int32_t rank0;                                   // tile-local rank of my first escape
     if (gs512) {
@@ -674,12 +659,8 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
       uint32_t* sw = s_warp[k & 1];
       if (lane == 31) sw[warp] = incl;
       asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
-      uint32_t v = lane < kWarps ? sw[lane] : 0u, vi = v;
-#pragma unroll
-      for (int o = 1; o < kWarps; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, vi, o);
-        vi += (lane >= o) ? u : 0u;
-      }
+      const uint32_t v = lane < kWarps ? sw[lane] : 0u;
+      const uint32_t vi = warp_incl_scan<kWarps>(v);
       const uint32_t wb = __shfl_sync(0xffffffffu, vi - v, warp);
       rank0 = (int32_t)(wb + wexcl);
       if (nv > 0 && (base & ((int64_t(1) << gsl) - 1)) == 0) {

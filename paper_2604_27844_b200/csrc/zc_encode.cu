@@ -198,12 +198,7 @@ encode_lookback_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs,
 
     // ---- tile-local exclusive scan of escape counts ------------------------
     const uint32_t cnt = __popc(esc);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
+    uint32_t incl = warp_incl_scan(cnt);
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();                                      // (B) s_warp, s_exp ready
     uint32_t wbase = 0, agg = 0;
@@ -409,21 +404,11 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       *reinterpret_cast<uint16_t*>(p_pl0 + 2 * pl_stride) = (uint16_t)prmt(A, B, 0x62);
       const uint32_t esc = prmt(A, B, 0x73) & 0xFFFFu;
       const uint32_t cnt = __popc(esc);
-      uint32_t incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        incl += (lane >= o) ? v : 0u;
-      }
+      uint32_t incl = warp_incl_scan(cnt);
       if (lane == 31) s_warp[warp] = incl;
       __syncthreads();                                    // (B)
       const uint32_t wv = lane < kWarps ? s_warp[lane] : 0u;
-      uint32_t wi = wv;
-#pragma unroll
-      for (int o = 1; o < kWarps; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
-        wi += (lane >= o) ? u : 0u;
-      }
+      uint32_t wi = warp_incl_scan<kWarps>(wv);
       const uint32_t wbase = __shfl_sync(0xffffffffu, wi - wv, warp);
       const uint32_t agg = __shfl_sync(0xffffffffu, wi, kWarps - 1);
       const uint32_t lp = run + wbase + incl - cnt;
@@ -545,20 +530,11 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
 
     // ---- tile-local scan ------------------------------------------------------
     const uint32_t cnt = __popc(esc);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      incl += (lane >= o) ? v : 0u;
-    }
+    uint32_t incl = warp_incl_scan(cnt);
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();                                      // (B)
-    uint32_t wv = lane < kWarps ? s_warp[lane] : 0u, wi = wv;
-#pragma unroll
-    for (int o = 1; o < kWarps; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
-      wi += (lane >= o) ? u : 0u;
-    }
+    const uint32_t wv = lane < kWarps ? s_warp[lane] : 0u;
+    const uint32_t wi = warp_incl_scan<kWarps>(wv);
     const uint32_t wbase = __shfl_sync(0xffffffffu, wi - wv, warp);
     const uint32_t agg = __shfl_sync(0xffffffffu, wi, kWarps - 1);
     const uint32_t lp = run + wbase + incl - cnt;   // run-relative escape prefix
