@@ -406,18 +406,38 @@ def run_ours(args):
             y = zc.decompress(chunk)                       # validated: err word read back
             return chunk, y
         # the caching allocator reaches its steady state (no cudaMalloc, which
-        # synchronises) after two calls; warm up like the device-timed leg
+        # synchronises) after two calls; each step drops the previous step's frame and output before it
+        # allocates, so the allocator hands back the same blocks every step
+        res = None
         for _ in range(max(3, args.warmup)):
-            api_step()
+            res = None
+            res = api_step()
         torch.cuda.synchronize()
+        a0 = torch.cuda.memory_stats().get("num_device_alloc", 0)
         ts = time.perf_counter()
         for _ in range(e_steps):
-            chunk, y = api_step()
+            res = None
+            res = api_step()
+        del res
         torch.cuda.synchronize()
         e_ms = (time.perf_counter() - ts) * 1e3 / e_steps
+        e_allocs = torch.cuda.memory_stats().get("num_device_alloc", 0) - a0
+        if os.environ.get("ZC_E2E_DEBUG"):
+            for _ in range(3):
+                t = [time.perf_counter()]
+                x = host.to(dev, non_blocking=True)
+                torch.cuda.synchronize(); t.append(time.perf_counter())
+                book = zc.codebook_for(x)
+                torch.cuda.synchronize(); t.append(time.perf_counter())
+                chunk = zc.compress(x, book)
+                torch.cuda.synchronize(); t.append(time.perf_counter())
+                y = zc.decompress(chunk)
+                torch.cuda.synchronize(); t.append(time.perf_counter())
+                print("e2e stages (h2d, book, compress, decompress) ms:",
+                      [round((b - a) * 1e3, 2) for a, b in zip(t, t[1:])], file=sys.stderr)
         e2e = {"value": 2 * LAYER_ELEMS / (e_ms / 1e3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 8 + 8 + 8 + 4,
-               "ms_per_step": e_ms,
+               "ms_per_step": e_ms, "device_allocs_in_timed_loop": e_allocs,
                "note": "H2D of the shard from pinned memory + codebook_for + compress + "
                        "decompress through the public API; reads back sigma-derived book, "
                        "frame length/zero_count and the decoder's error word"}

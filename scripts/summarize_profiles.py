@@ -27,10 +27,12 @@ def launches(tag):
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 items.append((d["Kernel Name"], float(d["Metric Value"])))
     zc = [(k, v) for k, v in items if k.startswith("zc::")]
-    # one bench step = stats (+finalize), encode (+fix-up), decode; take the last step
-    names = ["stats_kernel", "finalize_kernel", "encode_tiles_kernel", "encode_fixup_kernel",
-             "decode_ring_kernel"]
-    step = zc[-3:]
+    # one bench step = sums (certified statistic) [+ stats/finalize], encode
+    # (+ fused fix-up), decode: the zc:: launches from the last step's first kernel on
+    first = max(i for i, (k, _) in enumerate(zc)
+                if k.startswith("zc::sums_kernel") or k.startswith("zc::stats_kernel")
+                and not (i > 0 and zc[i - 1][0].startswith("zc::sums_kernel")))
+    step = zc[first:]
     total = sum(v for _, v in step)
     lines = [f"# launch list, one bench step (ncu gpu__time_duration, cold-cache, serialised)",
              f"# source: gpurun_out/launches_bench_{tag}.csv ({len(items)} launches)"]
@@ -84,7 +86,7 @@ if __name__ == "__main__":
     PROF.mkdir(exist_ok=True)
     launches(tag)
     traffic = {}
-    for k in ("decode_ring", "encode_tiles", "stats_kernel"):
+    for k in ("decode_ring", "encode_tiles", "sums_kernel"):
         b, t = kernel_summary(tag, k)
         traffic[f"{k if k.endswith('kernel') else k + '_kernel'}_per_launch_bytes"] = b
     traffic["source"] = f"ncu --set full captures prof_bench_{tag}_*.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum)"
