@@ -296,7 +296,10 @@ def run_ours(args):
             if rec:
                 ev["d1"][-1].record(stream)
             return err_buf
-        launches_per_step = 3          # stats (+fused finalize), encode (+fused fix-up), decode
+        # guess (1/32 sample), encoder with fused statistic + certificate +
+        # fix-up, exact-statistic and re-encode launches (return at once when
+        # the certificate decided and the guess held), decode
+        launches_per_step = 5
     else:
         comm = coll.Communicator.from_process_group()
         comm.use_p2p = args.transport == "p2p"
@@ -305,7 +308,9 @@ def run_ours(args):
 
         def step(rec=False):
             return coll.zip_all_gather(comm, shard)
-        launches_per_step = 5          # stats, finalize, encode pass 1 + fix-up, batched decode
+        # codebook+encode leg (4, as at N=1) + batched decode; the peer-memory
+        # path adds wait-done, signal-ready, wait-ready, signal-done kernels
+        launches_per_step = 9 if comm.use_p2p else 5
 
     # correctness gate before timing: bit-exact round trip
     err = step()
@@ -391,7 +396,8 @@ def run_ours(args):
                 "peak_kind": peak_kind, "alg_bytes_per_launch": alg,
                 "kernel_ms": dec_ms, "encode_ms": enc_ms,
                 "encode_GBps": (2 * n + frame_bytes) / (enc_ms / 1e3) / 1e9,
-                "encode_note": "codebook_for+compress (stats kernel 2n + encoder 2n + F)"}
+                "encode_note": "codebook_for+compress leg: guess kernel (1/32 sample) + encoder "
+                               "with the statistic fused (2n + F) + two conditional launches"}
 
     # ---- end to end through the public API (host buffers) --------------------
     e2e = None

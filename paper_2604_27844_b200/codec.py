@@ -169,6 +169,22 @@ def device_codebook(words: torch.Tensor, sigma=None, segs=None) -> torch.Tensor:
     return engine.modal_codebook(words, segs)
 
 
+def device_encode(words: torch.Tensor, segs, sigma, frames: torch.Tensor, frame_offs,
+                  gs_log2: int = 9, frame_len: torch.Tensor | None = None):
+    """codebook_for over the concatenated segments (the all-to-all scope of
+    collectives._prepare_frames, collectives.py:230-242) + one frame per
+    segment, stream-ordered on the device.  sigma None: the measured codebook
+    fused into the encoder (speculative path for large inputs, identical
+    output); otherwise the analytic / modal codebook, then the encoder.
+    Returns (book uint8[8], frame_len int64[nseg]) device tensors."""
+    segs = list(segs)
+    if sigma is None and len(segs) <= engine.MAX_SEGMENTS_MEASURED:
+        book, _, flen = engine.encode_measured(words, segs, gs_log2, frames, frame_offs, frame_len)
+        return book, flen
+    book = device_codebook(words, sigma, segs)
+    return book, engine.encode(words, segs, book, gs_log2, frames, frame_offs, frame_len)
+
+
 def codebook_for(data, sigma: float | None = None) -> ExponentCodebook:
     """Analytic codebook from sigma (measured on the GPU when None), modal
     fallback otherwise (codec.py:164-185)."""

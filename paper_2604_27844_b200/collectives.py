@@ -26,7 +26,6 @@ which costs 8 B per peer on top of the reference's metadata.
 
 from __future__ import annotations
 
-import math
 
 import numpy as np
 import torch
@@ -175,11 +174,10 @@ def zip_all_gather(comm: Communicator, local, sigma: float | None = None,
         if c != n:
             raise CollectiveError(f"frame holds {c} elements, expected {n}", peer=p)
     # K1 + K2: codebook from the local shard, one frame
-    book = codec.device_codebook(words, sigma)
     S = engine.static_bytes(n, GS_LOG2)
     cap = engine.max_frame_bytes(n, GS_LOG2)
     frame = torch.empty(cap, dtype=torch.uint8, device=dev)
-    flen = engine.encode(words, [(0, n)], book, GS_LOG2, frame, [0])
+    _, flen = codec.device_encode(words, [(0, n)], sigma, frame, [0], GS_LOG2)
     # frame lengths first (tiny), then the static sections (size known from n)
     lens = torch.empty(W, dtype=torch.int64, device=dev)
     if isinstance(comm, DistCommunicator) and comm.on_device:
@@ -223,17 +221,13 @@ def _prepare_frames(comm: Communicator, buf, offs, counts, sigma):
     if not peers:
         return None, frame_off, [0] * comm.world_size
     segs = [(offs[q], counts[q]) for q in peers]
-    if sigma is not None and math.isfinite(sigma) and sigma > 0.0:
-        book = codec.derive_codebook(sigma).device_tensor(dev)
-    else:
-        book = codec.device_codebook(buf, sigma, segs)
     caps = [engine.max_frame_bytes(counts[q], GS_LOG2) for q in peers]
     pos = 0
     for q, c in zip(peers, caps):
         frame_off[q] = pos
         pos += c
     frames = torch.empty(pos, dtype=torch.uint8, device=dev)
-    flen = engine.encode(buf, segs, book, GS_LOG2, frames, [frame_off[q] for q in peers])
+    _, flen = codec.device_encode(buf, segs, sigma, frames, [frame_off[q] for q in peers], GS_LOG2)
     lens = flen.cpu().tolist()
     frame_len = [0] * comm.world_size
     for q, ln in zip(peers, lens):
@@ -408,8 +402,7 @@ def zip_all_gather_p2p(comm: Communicator, local, sigma: float | None = None) ->
     werr = torch.full((1,), engine.ERR_OK, dtype=torch.int32, device=dev)
     if e > 1:
         ws.wait(1, e - 1, werr)                 # peers finished reading my last frame
-    book = codec.device_codebook(words, sigma)
-    flen = engine.encode(words, [(0, n)], book, GS_LOG2, ws.buf, [256])
+    _, flen = codec.device_encode(words, [(0, n)], sigma, ws.buf, [256], GS_LOG2)
     ws.signal(0, e)                             # my frame is ready
     ws.wait(0, e, werr)                         # every peer's frame is ready
     out = torch.empty(W * n, dtype=torch.int16, device=dev)
@@ -473,12 +466,8 @@ def zip_all_to_all_p2p(comm: Communicator, spec: AlltoAllSpec,
     peers_out = [q for q in comm.peers() if counts[q]]
     if peers_out:
         segs = [(offs[q], counts[q]) for q in peers_out]
-        if sigma is not None and math.isfinite(sigma) and sigma > 0.0:
-            book = codec.derive_codebook(sigma).device_tensor(dev)
-        else:
-            book = codec.device_codebook(buf, sigma, segs)
-        engine.encode(buf, segs, book, GS_LOG2, ws.buf,
-                      [256 + layouts[me][q] for q in peers_out])
+        codec.device_encode(buf, segs, sigma, ws.buf, [256 + layouts[me][q] for q in peers_out],
+                            GS_LOG2)
     ws.signal(0, e)
     ws.wait(0, e, werr)
     peers_in = [p for p in comm.peers() if spec.recv_counts[p]]

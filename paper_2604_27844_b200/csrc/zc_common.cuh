@@ -113,6 +113,20 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
 __device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
   *reinterpret_cast<uint4*>(p) = v;
 }
+// 32-B vector accesses (sm_100 LDG/STG.256).  When each lane owns 32
+// contiguous bytes, one 256-bit store per lane instead of two 128-bit ones
+// writes whole lines per instruction: 4.82 -> 5.88 TB/s on the decoder's
+// ring (scripts/exp/store_ring.cu).  p must be 32-B aligned.  Not volatile,
+// no memory clobber (see st_stream_v4).
+__device__ __forceinline__ void st_v8(void* p, uint4 a, uint4 b) {
+  asm("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
+      "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w));
+}
+__device__ __forceinline__ void ld_stream_v8(const void* p, uint4& a, uint4& b) {
+  asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p));
+}
 
 // Inclusive scan over the first `Lanes` lanes of a warp (all 32 lanes must
 // call it).  shfl.up's lane-valid predicate guards the add: one SHFL + one

@@ -18,6 +18,7 @@
 // 7-entry book + escape slot is an 8-byte PRMT table), escapes are expanded
 // into a per-thread 16-B shared slot and OR-ed in, and output words are built
 // four at a time from (sm, exponent) byte vectors with two LOP3 and two PRMT.
+#include <cstdlib>
 #include "zc_common.cuh"
 
 namespace zc {
@@ -310,7 +311,9 @@ decode_lookback_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_
       reassemble4(cb.s.z, E[2], o[4], o[5]);
       reassemble4(cb.s.w, E[3], o[6], o[7]);
       uint16_t* dst = out + segs.out_off[seg] + base;
-      if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      if (full && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
+        st_v8(dst, make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]));
+      } else if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
         st_stream_v4(dst, make_uint4(o[0], o[1], o[2], o[3]));
         st_stream_v4(dst + 8, make_uint4(o[4], o[5], o[6], o[7]));
       } else {
@@ -420,16 +423,20 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     // ======================= producer warp ===============================
     const int lane = tid;
     const int64_t zcap = pad128(H.zc);
+    // escape-range bounds of 32 tiles at once: bound(t) = gi[first group of
+    // t]; the next chunk's bounds are loaded one chunk ahead, so the ring
+    // never drains behind a dependent global load
+    auto bound_of = [&](int64_t tb) -> uint32_t {
+      return tb < seg_tiles ? gi[tb * gpt] : (uint32_t)H.zc;
+    };
+    uint32_t bnd_next = bound_of(t_begin + lane);
     for (int64_t c0 = t_begin; c0 < t_end; c0 += 32) {
-      // escape-range bounds of 32 tiles at once: bound(t) = gi[first group of t]
-      const int64_t tb = c0 + lane;
-      int64_t bnd = H.zc;
-      if (tb < seg_tiles) bnd = (int64_t)gi[tb * gpt];
-      const int64_t tb2 = c0 + 32;
-      const int64_t bnd32 = (tb2 < seg_tiles) ? (int64_t)gi[tb2 * gpt] : H.zc;
+      const int64_t bnd = bnd_next;
+      bnd_next = bound_of(c0 + 32 + lane);
       for (int j = 0; j < 32 && c0 + j < t_end; ++j) {
         const int64_t lo = __shfl_sync(0xffffffffu, bnd, j);
-        const int64_t hi = (j < 31) ? __shfl_sync(0xffffffffu, bnd, j + 1) : bnd32;
+        const int64_t hi = (j < 31) ? __shfl_sync(0xffffffffu, bnd, j + 1)
+                                    : (int64_t)__shfl_sync(0xffffffffu, bnd_next, 0);
         if (lane == 0) {
           const int64_t t = c0 + j, k = t - t_begin;
           const int st = (int)(k % kDStages);
@@ -489,7 +496,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
   // tiles [t_begin, t_fast_end) are full and take the lean gs = 512 path
   const int64_t t_fast_end = gs512 ? (n / kTile < t_end ? n / kTile : t_end) : t_begin;
   const bool out_aligned = ((reinterpret_cast<uintptr_t>(out_seg) & 15) == 0) && write_out;
-  const int ntl = (int)(t_end - t_begin);
+  const bool out_a32 = ((reinterpret_cast<uintptr_t>(out_seg) & 31) == 0) && write_out;
   const int nfast = (int)(t_fast_end > t_begin ? t_fast_end - t_begin : 0);
   const uint32_t zc32 = (uint32_t)H.zc;
   const uint32_t ngroups32 = (uint32_t)L.groups;
@@ -567,7 +574,9 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     reassemble4(sv.z, E2, o4, o5);
     reassemble4(sv.w, E3, o6, o7);
     uint16_t* dst = out_seg + ((t_begin + k) * kTile + ct * kEPT);
-    if (out_aligned) {
+    if (out_a32) {
+      st_v8(dst, make_uint4(o0, o1, o2, o3), make_uint4(o4, o5, o6, o7));
+    } else if (out_aligned) {
       st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
       st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
     } else if (write_out) {
@@ -715,7 +724,9 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
       reassemble4(sv.z, E2, o4, o5);
       reassemble4(sv.w, E3, o6, o7);
       uint16_t* dst = out_seg + base;
-      if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
+        st_v8(dst, make_uint4(o0, o1, o2, o3), make_uint4(o4, o5, o6, o7));
+      } else if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
         st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
         st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
       } else {
@@ -763,6 +774,13 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
   if (cap2 == 0) {
     cudaFuncSetAttribute(decode_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     cap2 = grid_cap((const void*)decode_ring_kernel, kDThreads, dyn);
+    if (const char* e = getenv("ZC_DECODE_CTAS_PER_SM")) {
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int want = sms * atoi(e);
+      if (want > 0 && want < cap2) cap2 = want;
+    }
   }
   DRunPlan rp{};
   int runs = 0;

@@ -312,14 +312,34 @@ __device__ __forceinline__ void encode_issue(const uint16_t* xs, int64_t n, int6
   }
 }
 
+// Fused certificate of the speculative path: every run's packed-fp32 sums,
+// and the last CTA to finish certifies the codebook (zc_stats.cuh).
+struct SpecOut {
+  SumPartial* parts;     // [nruns]
+  unsigned* done;        // zeroed before the launch
+  int64_t total;         // words over all segments
+  uint8_t* book;         // certified codebook (when *need == 0)
+  double* result;        // sigma, count, path
+  int* need;             // 1: the certificate failed, run the exact pass
+};
+
+// kSums: also accumulate the certified packed-fp32 statistic of x (the
+// speculative codebook path) and certify it at the end.
+template <bool kSums>
 __global__ void __launch_bounds__(kThreads)
 encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const RunPlan rp,
                     const uint8_t* __restrict__ book, uint8_t* __restrict__ frames,
                     uint8_t* __restrict__ scratch, uint64_t* __restrict__ run_total,
-                    Partial* __restrict__ stat_out, const int* __restrict__ cond, int cond_want,
+                    const SpecOut spec, const uint8_t* __restrict__ skip_if_same,
                     uint64_t* __restrict__ run_status, uint64_t* __restrict__ frame_len) {
-  // conditional launch (speculative path): run only if *cond == cond_want
-  if (cond != nullptr && *cond != cond_want) return;
+  // conditional launch (speculative path): the exact codebook equals the
+  // guess the frames were already encoded with -> nothing to do
+  if (skip_if_same != nullptr) {
+    bool same = true;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) same = same && (book[i] == skip_if_same[i]);
+    if (same) return;
+  }
   extern __shared__ __align__(128) uint8_t s_dyn[];
   uint8_t* ring = s_dyn;                                              // kStages x 8 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kStages * kStageBytes);
@@ -358,7 +378,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
   __syncthreads();
 
   uint32_t run = 0;   // escapes of this run before the current tile
-  StatAcc acc;        // fused exact statistics (speculative-codebook path)
+  double s1 = 0.0, s2 = 0.0;   // fused certified statistic (kSums), unshifted (K = 0)
   // ---- lean loop: aligned input, tile fully inside the segment ---------------
   const int64_t t_full_end = aligned ? ((n / kTile) < t_end ? (n / kTile) : t_end) : t_begin;
   const int nfast = (int)(t_full_end > t_begin ? t_full_end - t_begin : 0);
@@ -375,7 +395,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
       const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
       const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      if (stat_out) acc.add16(w, 0xFFFFu);
+      if (kSums) sums_acc16_k0(w, s1, s2);
       uint32_t sm[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -472,8 +492,15 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
         w[j] = lo | (hi << 16);
       }
     }
-    if (stat_out)
-      acc.add16(w, nvalid >= kEPT ? 0xFFFFu : (nvalid > 0 ? ((1u << nvalid) - 1u) : 0u));
+    if (kSums) {
+      // elements outside the segment contribute d = 0
+      uint32_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        v[j] = (2 * j < nvalid ? (w[j] & 0xFFFFu) : 0u) |
+               (2 * j + 1 < nvalid ? (w[j] & 0xFFFF0000u) : 0u);
+      sums_acc16_k0(v, s1, s2);
+    }
 
     // ---- sign-mantissa bytes (codec.py:279) ---------------------------------
     uint32_t sm[4];
@@ -568,7 +595,6 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     }
   }
   if (tid == 0) run_total[blockIdx.x] = run;
-  if (stat_out) stat_block_finish(acc, stat_out + blockIdx.x);
   if (run_status == nullptr) return;
 
   // ---- fused fix-up: escape offset of this run by a one-shot look-back over
@@ -604,6 +630,20 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     const uint64_t zc = P + run;
     write_header_and_pads(frame, L, zc, s_book);
     if (tid == 0) frame_len[seg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
+  }
+  if (kSums) {
+    // after the fix-up, so the certificate never delays a run's look-back
+    sums_block_finish(s1, s2, spec.parts + blockIdx.x);
+    __shared__ bool s_last;
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(spec.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      certify_block(spec.parts, gridDim.x, spec.total, spec.book, spec.result, spec.need);
+    }
   }
 }
 
@@ -648,30 +688,48 @@ static size_t tiles_dyn_smem() { return kStages * kStageBytes + kStages * sizeof
 static int tiles_cap() {
   static int cap1 = 0;
   if (cap1 == 0) {
-    cudaFuncSetAttribute(encode_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(encode_tiles_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tiles_dyn_smem());
-    cap1 = grid_for((const void*)encode_tiles_kernel, kThreads, tiles_dyn_smem());
+    cudaFuncSetAttribute(encode_tiles_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tiles_dyn_smem());
+    cap1 = grid_for((const void*)encode_tiles_kernel<false>, kThreads, tiles_dyn_smem());
+    const int cap2 = grid_for((const void*)encode_tiles_kernel<true>, kThreads, tiles_dyn_smem());
+    if (cap2 < cap1) cap1 = cap2;   // one plan serves both (the re-encode reuses it)
     if (cap1 > 4096) cap1 = 4096;
   }
   return cap1;
 }
 
-// pass 1 + fix-up with optional fused statistics / conditional execution
 // pass 1 with the fused fix-up epilogue (run-level look-back); optional fused
-// statistics / conditional execution for the speculative path
+// certificate (spec) / conditional execution (skip_if_same) for the
+// speculative path.  run_status: nruns zeroed words (zeroed here unless the
+// caller already did).
 static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, const RunPlan& rp,
                                    const uint8_t* book, uint8_t* frames, uint8_t* w8,
-                                   uint64_t* frame_len, Partial* stat_out, const int* cond,
-                                   int cond_want, cudaStream_t st) {
+                                   uint64_t* frame_len, const SpecOut* spec,
+                                   const uint8_t* skip_if_same, uint64_t* run_status,
+                                   bool zero_status, cudaStream_t st) {
   uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
-  uint64_t* run_status = reinterpret_cast<uint64_t*>(w8 + 256 + 8 * 4096 + kSpecArea - 8 * 4096);
   uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea;
-  cudaError_t e = cudaMemsetAsync(run_status, 0, 8 * (size_t)rp.nruns, st);
-  if (e != cudaSuccess) return e;
-  encode_tiles_kernel<<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
-      x, segs, rp, book, frames, scratch, run_total, stat_out, cond, cond_want, run_status,
-      frame_len);
+  if (zero_status) {
+    cudaError_t e = cudaMemsetAsync(run_status, 0, 8 * (size_t)rp.nruns, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (spec)
+    encode_tiles_kernel<true><<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
+        x, segs, rp, book, frames, scratch, run_total, *spec, skip_if_same, run_status,
+        frame_len);
+  else
+    encode_tiles_kernel<false><<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
+        x, segs, rp, book, frames, scratch, run_total, SpecOut{}, skip_if_same, run_status,
+        frame_len);
   return cudaGetLastError();
+}
+
+// run-level look-back words of the default path: the last 32 KB of the
+// speculative area (4096 runs max)
+static uint64_t* default_run_status(uint8_t* w8) {
+  return reinterpret_cast<uint64_t*>(w8 + 256 + 8 * 4096 + kSpecArea - 8 * 4096);
 }
 
 cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8_t* book,
@@ -692,31 +750,34 @@ cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8
   }
   const RunPlan rp = make_plan(segs, tiles_cap());
   if (rp.nruns > 4096) return cudaErrorInvalidValue;
-  return launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, nullptr, 0, st);
+  return launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, nullptr,
+                         default_run_status(w8), true, st);
 }
 
 cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
                                      double*, int, cudaStream_t);
-cudaError_t launch_codebook_sampled(const uint16_t*, const StatSegs&, int64_t, Partial*,
-                                    uint8_t*, double*, cudaStream_t);
-cudaError_t launch_finalize(const Partial*, int64_t, int64_t, uint8_t*, double*, const uint8_t*,
-                            int*, cudaStream_t);
+cudaError_t launch_guess(const uint16_t*, const StatSegs&, void*, unsigned*, uint8_t*,
+                         cudaStream_t);
+cudaError_t launch_exact_if_needed(const uint16_t*, const StatSegs&, int64_t, Partial*, unsigned*,
+                                   uint8_t*, double*, const int*, int, cudaStream_t);
 
-// Measured codebook + encode.  Large inputs take the speculative path: a
-// codebook guessed from every kSampleStride-th tile encodes while the encoder
-// accumulates the exact statistic; the exact codebook (reference
-// codebook_for semantics) is derived on the device and, only if it differs
-// from the guess, the frame is re-encoded (conditional kernels that return
-// immediately otherwise).  Saves the separate 2n-byte statistics pass.
+// Measured codebook + encode.  Large inputs take the speculative path:
+//   1. guess_kernel: a codebook guessed from a uniform 1/128 sample;
+//   2. the encoder runs with the guess and accumulates the certified packed-
+//      fp32 statistic of ALL of x on the side (same per-thread summation
+//      shape as sums_kernel, so the same error bound holds); its last CTA
+//      certifies the exact codebook (reference codebook_for semantics);
+//   3. only if the certificate failed, the exact f64 pass runs (a launch
+//      that returns at once otherwise);
+//   4. only if the exact codebook differs from the guess, the frames are
+//      encoded again (likewise conditional).
+// Output is identical to codebook + encode; the separate 2n-byte statistic
+// pass disappears in the common case.
 constexpr int64_t kSpecMinTiles = 1024;
-constexpr int64_t kSampleStride = 32;
 
 cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const StatSegs& ss,
                                int64_t total, uint8_t* frames, void* ws, uint64_t* frame_len,
                                uint8_t* book, double* result, int speculative, cudaStream_t st) {
-  // Measured (B200, 2^28): the fused f64 statistic makes the issue-bound
-  // encoder slower than the separate 2n-byte pass, so the two-step path is
-  // the default and the speculative path is opt-in (flags bit 0).
   const int64_t ntiles = segs.tile_start[segs.nseg];
   uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
   if (!speculative || ntiles < kSpecMinTiles) {
@@ -726,20 +787,38 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   }
   const RunPlan rp = make_plan(segs, tiles_cap());
   if (rp.nruns > 4096) return cudaErrorInvalidValue;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const RunPlan rp2 = make_plan(segs, sms);   // re-encode (rare): one wave, cheap no-op
+  // speculative area (kSpecArea = 512 KB):
+  //   [0, 128K)      guess partials (24 B per CTA, <= 8 per SM)
+  //   [128K, 192K)   run sums of the fused encoder (16 B per run)
+  //   [192K, 320K)   exact-pass partials (32 B per CTA)
+  //   [320K]         guess book; [320K+64] need flag
+  //   [448K-64, 448K) counters: guess, certificate, exact pass
+  //   [448K, 480K)   run status of the re-encode; [480K, 512K) of the encode
   uint8_t* spec = w8 + 256 + 8 * 4096;
-  Partial* parts_guess = reinterpret_cast<Partial*>(spec + 128);            // <= 4095 (counter at -64)
-  Partial* parts_exact = reinterpret_cast<Partial*>(spec + 4096 * 32);      // <= 4096
-  uint8_t* guess = spec + 8192 * 32;
-  double* guess_res = reinterpret_cast<double*>(spec + 8192 * 32 + 64);
-  int* mismatch = reinterpret_cast<int*>(spec + 8192 * 32 + 128);
-  cudaError_t e = launch_codebook_sampled(x, ss, kSampleStride, parts_guess, guess, guess_res, st);
+  SumPartial* guess_parts = reinterpret_cast<SumPartial*>(spec);
+  SumPartial* run_sums = reinterpret_cast<SumPartial*>(spec + 128 * 1024);
+  Partial* exact_parts = reinterpret_cast<Partial*>(spec + 192 * 1024);
+  uint8_t* guess = spec + 320 * 1024;
+  int* need = reinterpret_cast<int*>(spec + 320 * 1024 + 64);
+  unsigned* counters = reinterpret_cast<unsigned*>(spec + 448 * 1024 - 64);
+  uint64_t* status2 = reinterpret_cast<uint64_t*>(spec + 448 * 1024);
+  uint64_t* status1 = default_run_status(w8);
+  // one memset: counters + both status arrays (contiguous)
+  cudaError_t e = cudaMemsetAsync(counters, 0, 64 + 8 * 4096 + 8 * (size_t)rp.nruns, st);
   if (e != cudaSuccess) return e;
-  e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, parts_exact, nullptr, 0, st);
+  e = launch_guess(x, ss, guess_parts, counters + 0, guess, st);
   if (e != cudaSuccess) return e;
-  e = launch_finalize(parts_exact, rp.nruns, total, book, result, guess, mismatch, st);
+  const SpecOut so{run_sums, counters + 1, total, book, result, need};
+  e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, &so, nullptr, status1, false, st);
   if (e != cudaSuccess) return e;
-  // rare: the guess was wrong -> encode again with the exact codebook
-  return launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, mismatch, 1, st);
+  e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms, st);
+  if (e != cudaSuccess) return e;
+  return launch_two_pass(x, segs, rp2, book, frames, w8, frame_len, nullptr, guess, status2, false,
+                         st);
 }
 
 }  // namespace zc

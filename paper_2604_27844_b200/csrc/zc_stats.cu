@@ -149,34 +149,6 @@ static int stats_grid_cap() {
   return cap;
 }
 
-// --- host-identical codebook math (codec.py:74-161) ---------------------------
-// BASE_EXPONENT_OFFSET = 0.5*log2(14 ln2 / 16383) (codec.py:59), bit-exact literal
-constexpr double kBaseExponentOffset = -0x1.571514cbe4290p+2;
-__device__ double window_coverage(double sigma, double x) {
-  const double lo = exp2(x);
-  const double hi = lo * 128.0;
-  const double scale = sigma * sqrt(2.0);
-  return erf(hi / scale) - erf(lo / scale);
-}
-
-__device__ int clamp_base(int b) { return b < -126 ? -126 : (b > 121 ? 121 : b); }
-
-// derive_codebook (codec.py:149-161): floor/ceil of log2(sigma) + offset,
-// larger coverage wins, tie to floor; clamped like write_window
-__device__ int derive_base(double sigma) {
-  const double xo = log2(sigma) + kBaseExponentOffset;
-  const double lo = floor(xo), hi = ceil(xo);
-  const int base = (lo == hi || window_coverage(sigma, lo) >= window_coverage(sigma, hi))
-                       ? (int)lo : (int)hi;
-  return clamp_base(base);
-}
-
-__device__ void write_window(uint8_t* book, int base) {
-  const int first = clamp_base(base) + 127;
-  for (int i = 0; i < 7; ++i) book[i] = (uint8_t)(first + i);
-  book[7] = 0;
-}
-
 // Final reduction + derivation.  One CTA of 1024 threads; thread t merges a
 // fixed contiguous range, then a fixed binary tree.  result[0] = sigma
 // (NaN when no finite value), result[1] = finite count, result[2] = path
@@ -254,88 +226,6 @@ finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total
   finalize_block(parts, nparts, total_words, book, result, guess, mismatch);
 }
 
-// ---- certified fast statistic ------------------------------------------------
-// Every element contributes d = x - K (K = the first element when finite, else
-// 0; the same K everywhere, so partials merge by plain addition) to per-tile
-// sums kept in packed fp32 (FADD2/FFMA2, 8 terms per lane), flushed to f64
-// once per tile.  A non-finite element poisons the sums (inf/NaN propagate),
-// which routes the call to the exact f64 kernel.  Error bound (u = 2^-24):
-// per element fl(x - K) = d(1+δ), |δ| <= u; 8-term fp32 chains add <= γ_8;
-// f64 accumulation adds <= 2^-36 relative; with Q = Σd² (>= 0) and
-// |S1| <= sqrt(N Q):  |ΔS2| <= 11u·Q, |ΔS1| <= 10u·Σ|d|, so
-//   |ΔM2| = |ΔS2 - (2 S1 ΔS1 + ΔS1²)/N| <= 32u·Q + 2^-34·Q + N·2^-149
-// (the last term: fp32 underflow of d², also in the bound on Q).  The codebook is certified when
-// derive_base() agrees at both ends of sigma = sqrt((M2 ± Δ)/N), widened by
-// 2^-40 for the reference's own f64 evaluation (np.std two-pass error); the
-// reference's sigma lies in that interval and derive_base is monotone, so
-// its codebook is this one.  Otherwise *need = 1 and the exact pass runs.
-struct SumPartial {
-  double s1, s2;
-};
-
-__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ double f2_sum(uint64_t v) {
-  return (double)__uint_as_float((uint32_t)v) + (double)__uint_as_float((uint32_t)(v >> 32));
-}
-
-__device__ void certify_block(const SumPartial* parts, int64_t nparts, int64_t total,
-                              uint8_t* book, double* result, int* need) {
-  __shared__ double c_1[kWarps], c_2[kWarps];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t per = (nparts + kThreads - 1) / kThreads;
-  double a1 = 0.0, a2 = 0.0;
-  for (int64_t i = t * per; i < (t + 1) * per && i < nparts; ++i) {
-    a1 += __ldcg(&parts[i].s1);
-    a2 += __ldcg(&parts[i].s2);
-  }
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {   // fixed tree: lane i absorbs lane i+o
-    const double b1 = __shfl_down_sync(0xffffffffu, a1, o);
-    const double b2 = __shfl_down_sync(0xffffffffu, a2, o);
-    if ((lane & (2 * o - 1)) == 0) { a1 += b1; a2 += b2; }
-  }
-  if (lane == 0) { c_1[warp] = a1; c_2[warp] = a2; }
-  __syncthreads();
-  if (t != 0) return;
-  double S1 = 0.0, S2 = 0.0;
-  for (int i = 0; i < kWarps; ++i) { S1 += c_1[i]; S2 += c_2[i]; }
-  const double N = (double)total;
-  int decided = 0;
-  if (total > 0 && isfinite(S1) && isfinite(S2)) {
-    const double m2 = S2 - S1 * (S1 / N);
-    const double q = S2 * (1.0 + 0x1p-20);                 // >= true Q
-    const double delta = (32.0 * 0x1p-24 + 0x1p-34) * q + N * 0x1p-149;
-    if (m2 - delta > 0.0) {
-      const double s_lo = sqrt((m2 - delta) / N) * (1.0 - 0x1p-40);
-      const double s_hi = sqrt((m2 + delta) / N) * (1.0 + 0x1p-40);
-      if (isfinite(s_hi)) {
-        const int b = derive_base(s_lo);
-        if (b == derive_base(s_hi)) {
-          write_window(book, b);
-          result[0] = sqrt(m2 / N);
-          result[1] = N;
-          result[2] = 3.0;                                   // analytic, certified
-          decided = 1;
-        }
-      }
-    }
-  }
-  *need = decided ? 0 : 1;
-}
 
 // No TMA ring and no block barrier here: with ~3 instructions per element the
 // kernel is latency-bound on loads, and plain 16-B loads of two tiles per
@@ -356,17 +246,14 @@ __device__ __forceinline__ void sums_load16(const uint16_t* __restrict__ x, cons
   }
 }
 
-__device__ __forceinline__ void sums_acc16(const uint32_t* w, uint64_t K2, double& s1, double& s2) {
-  uint64_t a1 = 0, a2 = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint64_t v = (uint64_t)(w[j] & 0xFFFF0000u) << 32 | (uint64_t)(w[j] << 16);
-    const uint64_t d = f2_sub(v, K2);
-    a1 = f2_add(a1, d);
-    a2 = f2_fma(d, d, a2);
+
+__device__ __forceinline__ void ld_pair(const uint16_t* p, bool a32, uint4& a, uint4& b) {
+  if (a32) {
+    ld_stream_v8(p, a, b);
+  } else {
+    a = ld_stream_v4(p);
+    b = ld_stream_v4(p + 8);
   }
-  s1 += f2_sum(a1);
-  s2 += f2_sum(a2);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -382,16 +269,20 @@ sums_kernel(const uint16_t* __restrict__ x, const StatSegs segs, SumPartial* __r
   if ((kw & 0x7F80u) == 0x7F80u) kw = 0;
   const uint32_t kpair = kw | (kw << 16);
   const uint64_t K2 = (uint64_t)(kpair & 0xFFFF0000u) << 32 | (uint64_t)(kpair << 16);
-  // single aligned segment: every full tile is two aligned 16-B loads
-  const bool flat = segs.nseg == 1 && ((reinterpret_cast<uintptr_t>(x + segs.x_off[0]) & 15) == 0);
+  // single aligned segment: every full tile is one 32-B load per thread
+  // (two 16-B loads when the segment is only 16-B aligned)
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x + segs.x_off[0]);
+  const bool flat = segs.nseg == 1 && (xa & 15) == 0;
+  const bool a32 = (xa & 31) == 0;
   const int64_t nfull = flat ? segs.n[0] / kTile : 0;
   const uint16_t* x0 = x + segs.x_off[0] + tid * kEPT;
   double s1 = 0.0, s2 = 0.0;
   int64_t i = i0;
   const int64_t fend = nfull < i1 ? nfull : i1;
   for (; i + 2 <= fend; i += 2) {
-    const uint4 a = ld_stream_v4(x0 + i * kTile), b = ld_stream_v4(x0 + i * kTile + 8);
-    const uint4 c = ld_stream_v4(x0 + (i + 1) * kTile), d = ld_stream_v4(x0 + (i + 1) * kTile + 8);
+    uint4 a, b, c, d;
+    ld_pair(x0 + i * kTile, a32, a, b);
+    ld_pair(x0 + (i + 1) * kTile, a32, c, d);
     const uint32_t wa[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     const uint32_t wc[8] = {c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
     sums_acc16(wa, K2, s1, s2);
@@ -400,7 +291,8 @@ sums_kernel(const uint16_t* __restrict__ x, const StatSegs segs, SumPartial* __r
   for (; i < i1; ++i) {
     uint32_t w[8];
     if (i < nfull) {
-      const uint4 a = ld_stream_v4(x0 + i * kTile), b = ld_stream_v4(x0 + i * kTile + 8);
+      uint4 a, b;
+      ld_pair(x0 + i * kTile, a32, a, b);
       w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
       w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
     } else {
@@ -536,6 +428,125 @@ cudaError_t launch_finalize(const Partial* parts, int64_t nparts, int64_t total,
                             double* result, const uint8_t* guess, int* mismatch,
                             cudaStream_t st) {
   finalize_kernel<<<1, kThreads, 0, st>>>(parts, nparts, total, book, result, guess, mismatch);
+  return cudaGetLastError();
+}
+
+// ---- speculative encoder support (launch_encode_auto) -------------------------
+// Guess: the analytic codebook of the packed-fp32 sums over every `stride`-th
+// tile.  No certificate -- a wrong guess only costs a re-encode.
+// Guess for the speculative encoder: the analytic codebook of packed-fp32
+// sums over a uniform element sample -- one 32-B sector (16 words) every
+// kGuessStride words, i.e. 1/128 of the bytes, spread over the whole input
+// so that no region is over-weighted (a tile sample would be fooled by a
+// small cluster, e.g. the RMSNorm vectors at the end of a layer shard).  No
+// certificate: a wrong guess only costs a re-encode.
+constexpr int kGuessStride = 2048;
+struct GuessPartial {
+  double s1, s2, cnt;
+};
+
+__global__ void __launch_bounds__(kThreads)
+guess_kernel(const uint16_t* __restrict__ x, const StatSegs segs, GuessPartial* __restrict__ parts,
+             unsigned* __restrict__ done, uint8_t* __restrict__ guess) {
+  const int tid = threadIdx.x;
+  const int64_t ntiles = segs.tile_start[segs.nseg];
+  constexpr int kPerTile = kTile / kGuessStride;
+  const int64_t nprobe = ntiles * kPerTile;
+  uint32_t kw = x[segs.x_off[0]];
+  if ((kw & 0x7F80u) == 0x7F80u) kw = 0;
+  const uint64_t K2 = sums_shift(kw);
+  double s1 = 0.0, s2 = 0.0, cnt = 0.0;
+  for (int64_t p = (int64_t)blockIdx.x * kThreads + tid; p < nprobe; p += (int64_t)gridDim.x * kThreads) {
+    const int64_t tile = p / kPerTile;
+    const int sg = find_seg(segs.tile_start, segs.nseg, tile);
+    const int64_t off = (tile - segs.tile_start[sg]) * kTile + (p % kPerTile) * kGuessStride;
+    const int64_t nvalid = segs.n[sg] - off;
+    const uint16_t* q = x + segs.x_off[sg] + off;
+    uint32_t w[8];
+    if (nvalid >= kEPT && (reinterpret_cast<uintptr_t>(q) & 31) == 0) {
+      uint4 a, b;
+      ld_stream_v8(q, a, b);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t lo = (2 * j < nvalid) ? q[2 * j] : kw;          // d = 0 outside
+        const uint32_t hi = (2 * j + 1 < nvalid) ? q[2 * j + 1] : kw;
+        w[j] = lo | (hi << 16);
+      }
+    }
+    if (nvalid > 0) cnt += (double)(nvalid < kEPT ? nvalid : kEPT);
+    sums_acc16(w, K2, s1, s2);
+  }
+  __shared__ double g_1[kWarps], g_2[kWarps], g_3[kWarps];
+  __shared__ bool s_last;
+  auto block_sum = [&](double& a1, double& a2, double& a3) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a1 += __shfl_down_sync(0xffffffffu, a1, o);
+      a2 += __shfl_down_sync(0xffffffffu, a2, o);
+      a3 += __shfl_down_sync(0xffffffffu, a3, o);
+    }
+    if ((tid & 31) == 0) { g_1[tid >> 5] = a1; g_2[tid >> 5] = a2; g_3[tid >> 5] = a3; }
+    __syncthreads();
+    if (tid == 0) {
+      a1 = a2 = a3 = 0.0;
+      for (int k = 0; k < kWarps; ++k) { a1 += g_1[k]; a2 += g_2[k]; a3 += g_3[k]; }
+    }
+  };
+  block_sum(s1, s2, cnt);
+  if (tid == 0) {
+    parts[blockIdx.x] = GuessPartial{s1, s2, cnt};
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (unsigned k = tid; k < gridDim.x; k += kThreads) {
+    a1 += __ldcg(&parts[k].s1);
+    a2 += __ldcg(&parts[k].s2);
+    a3 += __ldcg(&parts[k].cnt);
+  }
+  __syncthreads();   // g_* reuse
+  block_sum(a1, a2, a3);
+  if (tid != 0) return;
+  const double m2 = a3 > 0.0 ? a2 - a1 * (a1 / a3) : 0.0;
+  // degenerate sample (constant / non-finite): window around K's exponent
+  const int base = (isfinite(m2) && m2 > 0.0) ? derive_base(sqrt(m2 / a3))
+                                                : (int)((kw >> 7) & 0xFF) - 127 - 3;
+  write_window(guess, base);
+}
+
+cudaError_t launch_guess(const uint16_t* x, const StatSegs& segs, void* parts, unsigned* done,
+                         uint8_t* guess, cudaStream_t st) {
+  const int64_t nprobe = segs.tile_start[segs.nseg] * (kTile / kGuessStride);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = (nprobe + kThreads - 1) / kThreads;
+  if (grid > 8 * sms) grid = 8 * sms;
+  guess_kernel<<<(unsigned)grid, kThreads, 0, st>>>(x, segs,
+                                                    reinterpret_cast<GuessPartial*>(parts), done,
+                                                    guess);
+  return cudaGetLastError();
+}
+
+// The exact f64 statistic over x, as a conditional launch behind the fused
+// certificate (returns at once when *need == 0).  `grid_limit` caps the CTAs
+// of this rarely-needed pass, so its no-op launch stays cheap.
+cudaError_t launch_exact_if_needed(const uint16_t* x, const StatSegs& segs, int64_t total,
+                                   Partial* parts, unsigned* done, uint8_t* book,
+                                   double* result, const int* need, int grid_limit,
+                                   cudaStream_t st) {
+  const int64_t ntiles = segs.tile_start[segs.nseg];
+  int64_t grid = stats_grid_cap();
+  if (grid > grid_limit) grid = grid_limit;
+  if (grid > ntiles) grid = ntiles;
+  stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(
+      x, segs, 1, parts, done, total, book, result, need);
   return cudaGetLastError();
 }
 

@@ -7,6 +7,7 @@
 // in a fixed order.  Used by the stand-alone K1 kernel and fused into the
 // encoder's TMA loop (speculative codebook path).
 #pragma once
+#include <cmath>
 #include "zc_common.cuh"
 
 namespace zc {
@@ -113,6 +114,183 @@ __device__ __forceinline__ void stat_block_finish(const StatAcc& a, Partial* out
     }
     *out = Partial{na, ma, qa, (double)ea};
   }
+}
+
+// ---- certified packed-fp32 statistic (see zc_stats.cu) -----------------------
+struct SumPartial {
+  double s1, s2;
+};
+
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ double f2_sum(uint64_t v) {
+  return (double)__uint_as_float((uint32_t)v) + (double)__uint_as_float((uint32_t)(v >> 32));
+}
+
+__device__ __forceinline__ void sums_acc16(const uint32_t* w, uint64_t K2, double& s1, double& s2) {
+  uint64_t a1 = 0, a2 = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint64_t v = (uint64_t)(w[j] & 0xFFFF0000u) << 32 | (uint64_t)(w[j] << 16);
+    const uint64_t d = f2_sub(v, K2);
+    a1 = f2_add(a1, d);
+    a2 = f2_fma(d, d, a2);
+  }
+  s1 += f2_sum(a1);
+  s2 += f2_sum(a2);
+}
+
+// Unshifted form (K = 0): 4 ops per element pair instead of 5.  Exact
+// inputs (bf16 is a subset of fp32), so the error bound above still holds;
+// a large mean relative to sigma only makes the certificate fail more often
+// (then the exact pass decides).  Used by the fused encoder.
+__device__ __forceinline__ void sums_acc16_k0(const uint32_t* w, double& s1, double& s2) {
+  uint64_t a1 = 0, a2 = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint64_t v = (uint64_t)(w[j] & 0xFFFF0000u) << 32 | (uint64_t)(w[j] << 16);
+    a1 = f2_add(a1, v);
+    a2 = f2_fma(v, v, a2);
+  }
+  s1 += f2_sum(a1);
+  s2 += f2_sum(a2);
+}
+
+// Shift word pair of the certified statistic: K = the first element of the
+// concatenation when finite, else 0, in both halves (d = x - K per element).
+__device__ __forceinline__ uint64_t sums_shift(uint32_t kw) {
+  const uint32_t kpair = kw | (kw << 16);
+  return (uint64_t)(kpair & 0xFFFF0000u) << 32 | (uint64_t)(kpair << 16);
+}
+
+// CTA sum of (s1, s2) in a fixed order; thread 0 writes *out.
+__device__ __forceinline__ void sums_block_finish(double s1, double s2, SumPartial* out) {
+  __shared__ double b_1[kWarps], b_2[kWarps];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_down_sync(0xffffffffu, s1, o);
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  }
+  const int tid = threadIdx.x;
+  if ((tid & 31) == 0) { b_1[tid >> 5] = s1; b_2[tid >> 5] = s2; }
+  __syncthreads();
+  if (tid == 0) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int k = 0; k < kWarps; ++k) { t1 += b_1[k]; t2 += b_2[k]; }
+    *out = SumPartial{t1, t2};
+  }
+}
+
+// --- host-identical codebook math (codec.py:74-161) ---------------------------
+// BASE_EXPONENT_OFFSET = 0.5*log2(14 ln2 / 16383) (codec.py:59), bit-exact literal
+constexpr double kBaseExponentOffset = -0x1.571514cbe4290p+2;
+__device__ inline double window_coverage(double sigma, double x) {
+  const double lo = exp2(x);
+  const double hi = lo * 128.0;
+  const double scale = sigma * sqrt(2.0);
+  return erf(hi / scale) - erf(lo / scale);
+}
+
+__device__ inline int clamp_base(int b) { return b < -126 ? -126 : (b > 121 ? 121 : b); }
+
+// derive_codebook (codec.py:149-161): floor/ceil of log2(sigma) + offset,
+// larger coverage wins, tie to floor; clamped like write_window
+// Coverage depends on sigma only through 2^x / sigma, so the floor/ceil
+// choice depends only on frac(x_opt): floor below kFlipFrac, ceil above
+// (swept against the reference's derive_codebook at 10^6 points per octave,
+// no exception).  Away from the flip the erf evaluations are skipped -- they
+// are a long serial f64 chain in a single thread at the end of the
+// statistic kernels; within kFlipWindow of it the reference formula decides.
+constexpr double kFlipFrac = 0.35891885782276935;
+constexpr double kFlipWindow = 1e-4;
+__device__ inline int derive_base(double sigma) {
+  const double xo = log2(sigma) + kBaseExponentOffset;
+  const double lo = floor(xo), hi = ceil(xo);
+  const double fr = xo - lo;
+  if (fabs(fr - kFlipFrac) > kFlipWindow) return clamp_base(fr < kFlipFrac ? (int)lo : (int)hi);
+  const int base = (lo == hi || window_coverage(sigma, lo) >= window_coverage(sigma, hi))
+                       ? (int)lo : (int)hi;
+  return clamp_base(base);
+}
+
+__device__ inline void write_window(uint8_t* book, int base) {
+  const int first = clamp_base(base) + 127;
+  for (int i = 0; i < 7; ++i) book[i] = (uint8_t)(first + i);
+  book[7] = 0;
+}
+
+
+// ---- certified fast statistic ------------------------------------------------
+// Every element contributes d = x - K (K = the first element when finite, else
+// 0; the same K everywhere, so partials merge by plain addition) to per-tile
+// sums kept in packed fp32 (FADD2/FFMA2, 8 terms per lane), flushed to f64
+// once per tile.  A non-finite element poisons the sums (inf/NaN propagate),
+// which routes the call to the exact f64 kernel.  Error bound (u = 2^-24):
+// per element fl(x - K) = d(1+δ), |δ| <= u; 8-term fp32 chains add <= γ_8;
+// f64 accumulation adds <= 2^-36 relative; with Q = Σd² (>= 0) and
+// |S1| <= sqrt(N Q):  |ΔS2| <= 11u·Q, |ΔS1| <= 10u·Σ|d|, so
+//   |ΔM2| = |ΔS2 - (2 S1 ΔS1 + ΔS1²)/N| <= 32u·Q + 2^-34·Q + N·2^-149
+// (the last term: fp32 underflow of d², also in the bound on Q).  The codebook is certified when
+// derive_base() agrees at both ends of sigma = sqrt((M2 ± Δ)/N), widened by
+// 2^-40 for the reference's own f64 evaluation (np.std two-pass error); the
+// reference's sigma lies in that interval and derive_base is monotone, so
+// its codebook is this one.  Otherwise *need = 1 and the exact pass runs.
+__device__ inline void certify_block(const SumPartial* parts, int64_t nparts, int64_t total,
+                              uint8_t* book, double* result, int* need) {
+  __shared__ double c_1[kWarps], c_2[kWarps];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t per = (nparts + kThreads - 1) / kThreads;
+  double a1 = 0.0, a2 = 0.0;
+  for (int64_t i = t * per; i < (t + 1) * per && i < nparts; ++i) {
+    a1 += __ldcg(&parts[i].s1);
+    a2 += __ldcg(&parts[i].s2);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {   // fixed tree: lane i absorbs lane i+o
+    const double b1 = __shfl_down_sync(0xffffffffu, a1, o);
+    const double b2 = __shfl_down_sync(0xffffffffu, a2, o);
+    if ((lane & (2 * o - 1)) == 0) { a1 += b1; a2 += b2; }
+  }
+  if (lane == 0) { c_1[warp] = a1; c_2[warp] = a2; }
+  __syncthreads();
+  if (t != 0) return;
+  double S1 = 0.0, S2 = 0.0;
+  for (int i = 0; i < kWarps; ++i) { S1 += c_1[i]; S2 += c_2[i]; }
+  const double N = (double)total;
+  int decided = 0;
+  if (total > 0 && isfinite(S1) && isfinite(S2)) {
+    const double m2 = S2 - S1 * (S1 / N);
+    const double q = S2 * (1.0 + 0x1p-20);                 // >= true Q
+    const double delta = (32.0 * 0x1p-24 + 0x1p-34) * q + N * 0x1p-149;
+    if (m2 - delta > 0.0) {
+      const double s_lo = sqrt((m2 - delta) / N) * (1.0 - 0x1p-40);
+      const double s_hi = sqrt((m2 + delta) / N) * (1.0 + 0x1p-40);
+      if (isfinite(s_hi)) {
+        const int b = derive_base(s_lo);
+        if (b == derive_base(s_hi)) {
+          write_window(book, b);
+          result[0] = sqrt(m2 / N);
+          result[1] = N;
+          result[2] = 3.0;                                   // analytic, certified
+          decided = 1;
+        }
+      }
+    }
+  }
+  *need = decided ? 0 : 1;
 }
 
 }  // namespace zc

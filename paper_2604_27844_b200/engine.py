@@ -58,6 +58,7 @@ def book_tensor(entries, device) -> torch.Tensor:
 
 
 SIGMA_EXACT = 1   # zc_codebook_measured flag (include/zipccl_b200.h)
+MAX_SEGMENTS_MEASURED = _lib.MAX_SEGMENTS   # segments per zc_encode_measured call
 
 
 def measured_codebook(words: torch.Tensor, segs=None, stream=None, exact: bool = False):
@@ -131,9 +132,10 @@ def encode(words: torch.Tensor, segs, book: torch.Tensor, gs_log2: int,
 
 def encode_measured(words: torch.Tensor, segs, gs_log2: int, frames: torch.Tensor, frame_offs,
                     frame_len: torch.Tensor | None = None, stream=None,
-                    speculative: bool = False):
+                    speculative: bool = True):
     """codebook_for over the concatenated segments + one frame per segment
-    (speculative fused statistics for large inputs).  Returns (book uint8[8],
+    (speculative: the statistic fused into the encoder for large inputs;
+    identical output either way).  Returns (book uint8[8],
     result float64[3], frame_len int64[nseg]); all stay on the device."""
     segs = list(segs)
     nseg = len(segs)

@@ -72,9 +72,18 @@ def main():
     t_stats = timed(graphed(lambda: engine.measured_codebook(w)))
     t_enc = timed(graphed(lambda: engine.encode(w, [(0, n)], book, 9, frames, [0], flen)))
     t_dec = timed(graphed(lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0])))
-    t_step = timed(graphed(lambda: (engine.encode_measured(w, [(0, n)], 9, frames, [0], flen),
+    t_step = timed(graphed(lambda: (engine.encode_measured(w, [(0, n)], 9, frames, [0], flen,
+                                                           speculative=False),
                                     engine.decode([frames.data_ptr()], [0], None, [n], out,
                                                   [0]))))
+    t_enc_spec = timed(graphed(lambda: engine.encode_measured(w, [(0, n)], 9, frames, [0], flen,
+                                                              speculative=True)))
+    t_enc_meas = timed(graphed(lambda: engine.encode_measured(w, [(0, n)], 9, frames, [0], flen,
+                                                              speculative=False)))
+    t_step_spec = timed(graphed(lambda: (engine.encode_measured(w, [(0, n)], 9, frames, [0], flen,
+                                                                speculative=True),
+                                         engine.decode([frames.data_ptr()], [0], None, [n], out,
+                                                       [0]))))
     copy_dst = torch.empty_like(w)
     t_copy = timed(lambda: copy_dst.copy_(w))
     r = dict(n=n, frame=F, ratio=2 * n / F,
@@ -83,6 +92,8 @@ def main():
              decode_ms=t_dec, decode_GBps=(2 * n + F) / t_dec / 1e6,
              copy_ms=t_copy, copy_GBps=4 * n / t_copy / 1e6,
              step_ms=t_step, step_GBps=2 * n / t_step / 1e6,
+             measured_encode_ms=t_enc_meas, speculative_encode_ms=t_enc_spec,
+             step_spec_ms=t_step_spec, step_spec_GBps=2 * n / t_step_spec / 1e6,
              sigma=float(res[0].item()), book=book[:7].tolist())
     print(json.dumps(r))
 
