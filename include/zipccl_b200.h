@@ -31,6 +31,16 @@ extern "C" {
 
 /* ABI version (1). */
 int zc_abi_version(void);
+/* Kernel timing hooks (measurement only).  zc_profile_enable(1) resets and
+ * starts recording CUDA events on the launching stream around every pass-1
+ * encoder launch (tag 0; zc_encode / zc_encode_measured) and every decoder
+ * launch (tag 1; zc_decode); zc_profile_enable(0) stops.  Never enable while
+ * a stream is being captured into a CUDA graph.  zc_profile_read waits for
+ * the recorded events and writes up to `cap` launch durations (ms) of `tag`
+ * into ms; returns how many (or a negative status). */
+int zc_profile_enable(int on);
+int zc_profile_read(int tag, float* ms, int cap);
+
 /* Elements per CTA tile of the encode/decode/stats kernels (4096). */
 int zc_tile_elements(void);
 /* Segments accepted per batched call (64). */

@@ -30,6 +30,8 @@ _P = ctypes.POINTER
 
 EXPORTS = {
     "zc_abi_version": (_int, []),
+    "zc_profile_enable": (_int, [_int]),
+    "zc_profile_read": (_int, [_int, _P(ctypes.c_float), _int]),
     "zc_tile_elements": (_int, []),
     "zc_max_segments": (_int, []),
     "zc_status_string": (ctypes.c_char_p, [_int]),

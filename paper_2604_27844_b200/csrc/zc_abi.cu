@@ -2,6 +2,8 @@
 // Plain pointers and sizes only; all device work is enqueued on the caller's
 // stream and nothing here synchronises.
 #include <cstring>
+#include <mutex>
+#include <vector>
 #include "zc_common.cuh"
 
 namespace zc {
@@ -19,6 +21,36 @@ cudaError_t launch_encode_auto(const uint16_t*, const EncodeSegs&, const StatSeg
 
 using namespace zc;
 
+namespace zc {
+namespace {
+struct ProfState {
+  std::mutex m;
+  bool on = false;
+  std::vector<cudaEvent_t> ev[kProfTags];   // begin/end pairs
+  size_t used[kProfTags] = {0, 0};
+};
+ProfState g_prof;
+constexpr size_t kProfMaxPairs = 4096;
+}  // namespace
+
+void prof_mark(int tag, bool end, cudaStream_t st) {
+  if (!g_prof.on) return;
+  std::lock_guard<std::mutex> lk(g_prof.m);
+  if (!g_prof.on || tag < 0 || tag >= kProfTags) return;
+  auto& v = g_prof.ev[tag];
+  size_t& u = g_prof.used[tag];
+  if (u >= kProfMaxPairs) return;
+  const size_t i = 2 * u + (end ? 1 : 0);
+  while (v.size() <= i) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    v.push_back(e);
+  }
+  cudaEventRecord(v[i], st);
+  if (end) ++u;
+}
+}  // namespace zc
+
 namespace {
 constexpr int kStatusBadArg = -1;
 constexpr int kStatusWorkspace = -2;
@@ -32,6 +64,27 @@ int status_of(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
 extern "C" {
 
 int zc_abi_version(void) { return 2; }
+
+int zc_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof.m);
+  g_prof.on = on != 0;
+  if (g_prof.on)
+    for (int t = 0; t < kProfTags; ++t) g_prof.used[t] = 0;
+  return 0;
+}
+
+int zc_profile_read(int tag, float* ms, int cap) {
+  if (tag < 0 || tag >= kProfTags || (!ms && cap > 0)) return kStatusBadArg;
+  std::lock_guard<std::mutex> lk(g_prof.m);
+  const size_t n = g_prof.used[tag] < (size_t)cap ? g_prof.used[tag] : (size_t)cap;
+  for (size_t i = 0; i < n; ++i) {
+    cudaEvent_t a = g_prof.ev[tag][2 * i], b = g_prof.ev[tag][2 * i + 1];
+    cudaError_t e = cudaEventSynchronize(b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(ms + i, a, b);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return (int)n;
+}
 
 int zc_tile_elements(void) { return kTile; }
 

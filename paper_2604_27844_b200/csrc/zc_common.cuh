@@ -115,8 +115,9 @@ __device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
 }
 // 32-B vector accesses (sm_100 LDG/STG.256).  When each lane owns 32
 // contiguous bytes, one 256-bit store per lane instead of two 128-bit ones
-// writes whole lines per instruction: 4.82 -> 5.88 TB/s on the decoder's
-// ring (scripts/exp/store_ring.cu).  p must be 32-B aligned.  Not volatile,
+// writes whole lines per instruction: 4.82 -> 5.88 TB/s on the store-ring
+// micro-benchmark (scripts/exp/store_ring.cu; the decoder itself gains ~1%,
+// its consumers' latency dominates).  p must be 32-B aligned.  Not volatile,
 // no memory clobber (see st_stream_v4).
 __device__ __forceinline__ void st_v8(void* p, uint4 a, uint4 b) {
   asm("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
@@ -286,6 +287,13 @@ struct DecodeSegs {
   int64_t n[kMaxSegments];                // expected element count
   int64_t out_off[kMaxSegments];          // element offset into out
 };
+
+// Kernel timing hooks (zc_profile_enable / zc_profile_read in the C-ABI):
+// when enabled, CUDA events are recorded on the launching stream right
+// before and after the pass-1 encoder and the decoder launches.  No-ops
+// otherwise (and never enable them while a stream is being captured).
+enum ProfTag { kProfEncode = 0, kProfDecode = 1, kProfTags = 2 };
+void prof_mark(int tag, bool end, cudaStream_t st);
 
 __device__ __forceinline__ int find_seg(const int64_t* tile_start, int nseg, int64_t tile) {
   int s = 0;

@@ -766,7 +766,9 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
     static int cap = 0;
     if (cap == 0) cap = grid_cap((const void*)decode_lookback_kernel, kThreads, 0);
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    prof_mark(kProfDecode, false, st);
     decode_lookback_kernel<<<grid, kThreads, 0, st>>>(segs, out, err, status, counter, write_out);
+    prof_mark(kProfDecode, true, st);
     return cudaGetLastError();
   }
   const size_t dyn = kDStages * kDStageBytes + 2 * kDStages * sizeof(uint64_t);
@@ -795,7 +797,9 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
   }
   rp.run_start[segs.nseg] = runs;
   rp.nruns = runs;
+  prof_mark(kProfDecode, false, st);
   decode_ring_kernel<<<runs, kDThreads, dyn, st>>>(segs, rp, out, err, write_out);
+  prof_mark(kProfDecode, true, st);
   return cudaGetLastError();
 }
 

@@ -715,6 +715,8 @@ static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, co
     cudaError_t e = cudaMemsetAsync(run_status, 0, 8 * (size_t)rp.nruns, st);
     if (e != cudaSuccess) return e;
   }
+  const bool timed = skip_if_same == nullptr;   // not the conditional re-encode
+  if (timed) prof_mark(kProfEncode, false, st);
   if (spec)
     encode_tiles_kernel<true><<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
         x, segs, rp, book, frames, scratch, run_total, *spec, skip_if_same, run_status,
@@ -723,6 +725,7 @@ static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, co
     encode_tiles_kernel<false><<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
         x, segs, rp, book, frames, scratch, run_total, SpecOut{}, skip_if_same, run_status,
         frame_len);
+  if (timed) prof_mark(kProfEncode, true, st);
   return cudaGetLastError();
 }
 

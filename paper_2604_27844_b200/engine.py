@@ -185,6 +185,25 @@ def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_
     return err
 
 
+PROF_ENCODE, PROF_DECODE = 0, 1
+
+
+def profile_enable(on: bool) -> None:
+    """Start (reset) / stop recording CUDA events around every pass-1 encoder
+    and decoder launch (zc_profile_enable).  Eager launches only."""
+    lib().zc_profile_enable(1 if on else 0)
+
+
+def profile_read(tag: int, cap: int = 4096) -> list:
+    """Durations (ms) of the launches recorded for `tag` since profile_enable."""
+    import ctypes
+    buf = (ctypes.c_float * cap)()
+    k = lib().zc_profile_read(int(tag), buf, cap)
+    if k < 0:
+        raise RuntimeError(f"zc_profile_read failed: status {k}")
+    return [float(buf[i]) for i in range(k)]
+
+
 ERR_OK = 0x7F7F7F7F
 
 # error code -> (field, detail) in reference wording (container.py:113-180,

@@ -26,18 +26,19 @@ def launches(tag):
             d = dict(zip(hdr, r))
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 items.append((d["Kernel Name"], float(d["Metric Value"])))
+    items = [(k[5:] if k.startswith("void ") else k, v) for k, v in items]
     zc = [(k, v) for k, v in items if k.startswith("zc::")]
-    # one bench step = sums (certified statistic) [+ stats/finalize], encode
-    # (+ fused fix-up), decode: the zc:: launches from the last step's first kernel on
-    first = max(i for i, (k, _) in enumerate(zc)
-                if k.startswith("zc::sums_kernel") or k.startswith("zc::stats_kernel")
-                and not (i > 0 and zc[i - 1][0].startswith("zc::sums_kernel")))
-    step = zc[first:]
+    # one bench step = guess, encoder (fused statistic + certificate + fix-up),
+    # two conditional launches, decode: the zc:: launches from the last guess on
+    first = max(i for i, (k, _) in enumerate(zc) if k.startswith("zc::guess_kernel"))
+    last = next(i for i in range(first, len(zc)) if zc[i][0].startswith("zc::decode_ring"))
+    step = zc[first:last + 1]
     total = sum(v for _, v in step)
     lines = [f"# launch list, one bench step (ncu gpu__time_duration, cold-cache, serialised)",
              f"# source: gpurun_out/launches_bench_{tag}.csv ({len(items)} launches)"]
     for k, v in step:
-        lines.append(f"{k.split('(')[0]:<32} {v / 1e3:9.1f} us  {100 * v / total:5.1f}% of step")
+        name = k.split('(')[0].replace("void ", "")
+        lines.append(f"{name:<36} {v / 1e3:9.1f} us  {100 * v / total:5.1f}% of step")
     lines.append(f"{'step total':<32} {total / 1e3:9.1f} us")
     (PROF / f"{tag}_launches.txt").write_text("\n".join(lines) + "\n")
     return step
@@ -86,7 +87,7 @@ if __name__ == "__main__":
     PROF.mkdir(exist_ok=True)
     launches(tag)
     traffic = {}
-    for k in ("decode_ring", "encode_tiles", "sums_kernel"):
+    for k in ("decode_ring", "encode_tiles", "guess_kernel"):
         b, t = kernel_summary(tag, k)
         traffic[f"{k if k.endswith('kernel') else k + '_kernel'}_per_launch_bytes"] = b
     traffic["source"] = f"ncu --set full captures prof_bench_{tag}_*.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum)"

@@ -297,3 +297,21 @@ def test_speculative_multi_segment_matches_prepare_frames(golden_meta):
     fl = flen.cpu().tolist()
     for k, q in enumerate([0, 2, 3]):
         assert host[foffs[k]:foffs[k] + fl[k]].tobytes() == expect[q], q
+
+
+def test_profile_hooks_record_encoder_and_decoder_launches():
+    n = 4096 * 1200 + 5
+    x = engine.words_view((torch.randn(n, device="cuda") * 0.02).to(torch.bfloat16))
+    frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(x)
+    engine.profile_enable(True)
+    try:
+        for _ in range(3):
+            engine.encode_measured(x, [(0, n)], 9, frames, [0])
+            engine.decode([frames.data_ptr()], [0], None, [n], out, [0])
+    finally:
+        engine.profile_enable(False)
+    enc, dec = engine.profile_read(engine.PROF_ENCODE), engine.profile_read(engine.PROF_DECODE)
+    assert len(enc) == 3 and len(dec) == 3
+    assert all(t > 0 for t in enc + dec)
+    assert torch.equal(out, x)

@@ -138,3 +138,48 @@ def test_certified_multi_segment_and_unaligned():
     assert tuple(book[:7].tolist()) == zo.book_for(concat)
     assert res[1].item() == concat.size
     assert res[0].item() == pytest.approx(zo.sigma(concat), rel=4e-6)
+
+
+@pytest.mark.parametrize("rel", [2e-5, -2e-5, 5e-4, -5e-4, 3e-3, -3e-3])
+def test_exact_derivation_both_sides_of_flip_window(rel):
+    # the device derivation skips the erf comparison when frac(x_opt) is more
+    # than kFlipWindow (1e-4) from the flip; these straddle that window
+    target = _flip_sigma(-7)
+    host = _three_point(target, 1 << 20, rel, seed=7)
+    x = torch.from_numpy(host.view(np.int16)).cuda()
+    book, res = engine.measured_codebook(x, exact=True)
+    assert tuple(book[:7].tolist()) == zo.book_for(host), (rel, res.tolist())
+
+
+def _speculative(host: np.ndarray):
+    x = torch.from_numpy(host.view(np.int16)).cuda()
+    n = host.size
+    frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    book, res, flen = engine.encode_measured(x, [(0, n)], 9, frames, [0], speculative=True)
+    frame = frames[:int(flen.item())].cpu().numpy().tobytes()
+    return tuple(book[:7].tolist()), res.cpu().tolist(), frame
+
+
+@pytest.mark.parametrize("rel", [1e-8, -1e-8, 3e-7, -3e-7])
+def test_speculative_near_flip_falls_back_to_exact(rel):
+    # above the speculative threshold; the fused certificate must refuse and
+    # the exact pass (then a re-encode when the guess was wrong) decides
+    target = _flip_sigma(-6)
+    host = _three_point(target, 1 << 23, rel, seed=11)
+    book, res, frame = _speculative(host)
+    assert book == zo.book_for(host)
+    assert res[2] == PATH_EXACT, res
+    assert frame == zo.encode(host, book)
+
+
+def test_speculative_cluster_outside_sample_grid():
+    # layer-like: N(0, 0.02^2) weights + a block of 1.0 (RMSNorm) at the end;
+    # a tile sample would over-weight the block, the uniform sample must not
+    # (either way the output is exact)
+    n = (1 << 23) + 8192
+    host = zo.gaussian(n, 0.02, seed=4)
+    host[-8192:] = 0x3F80
+    book, res, frame = _speculative(host)
+    assert book == zo.book_for(host)
+    assert res[2] == PATH_CERTIFIED, res
+    assert frame == zo.encode(host, book)
