@@ -61,6 +61,7 @@ int64_t tiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
 int status_of(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
 }  // namespace
 
+
 extern "C" {
 
 int zc_abi_version(void) { return 2; }

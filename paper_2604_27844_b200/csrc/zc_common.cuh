@@ -293,6 +293,29 @@ struct DecodeSegs {
 // before and after the pass-1 encoder and the decoder launches.  No-ops
 // otherwise (and never enable them while a stream is being captured).
 enum ProfTag { kProfEncode = 0, kProfDecode = 1, kProfTags = 2 };
+
+// Per-CTA %globaltimer stamps for load-balance experiments; compiled only
+// into the -DZC_TIMELINE debug library (scripts/exp/timeline.py).  One copy
+// per translation unit (no -rdc), read by zc_debug_timeline_{enc,dec}.
+#ifdef ZC_TIMELINE
+constexpr int kTlSlots = 6, kTlCtas = 8192;
+static __device__ unsigned long long zc_tl[kTlSlots][kTlCtas];
+#define ZC_TL_EXPORT(name)                                                   \
+  extern "C" int name(unsigned long long* host) {                            \
+    return (int)cudaMemcpyFromSymbol(host, zc::zc_tl, sizeof(zc::zc_tl));     \
+  }
+#define ZC_TL(slot, thread)                                                  \
+  do {                                                                       \
+    if (threadIdx.x == (thread) && blockIdx.x < kTlCtas) {                   \
+      unsigned long long t_;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      zc_tl[slot][blockIdx.x] = t_;                                          \
+    }                                                                        \
+  } while (0)
+#else
+#define ZC_TL(slot, thread) do {} while (0)
+#define ZC_TL_EXPORT(name)
+#endif
 void prof_mark(int tag, bool end, cudaStream_t st);
 
 __device__ __forceinline__ int find_seg(const int64_t* tile_start, int nseg, int64_t tile) {

@@ -345,7 +345,17 @@ decode_lookback_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_
 // reference's diff(gi) == per-group escapes, gi[0] == 0, sum == zero_count.
 // ============================================================================
 
-constexpr int kDStages = 4;
+#ifndef ZC_DSTAGES
+#define ZC_DSTAGES 4
+#endif
+#ifndef ZC_DMINB
+#define ZC_DMINB 3
+#endif
+#ifndef ZC_DCHUNK
+#define ZC_DCHUNK 4
+#endif
+constexpr int kDStages = ZC_DSTAGES;
+constexpr int kDChunk = ZC_DCHUNK;                  // tiles per dynamic claim
 constexpr int kGiSlots = 264;                       // up to 257 gi entries (gs >= 16) + align
 constexpr int kEscSlots = kTile + 32;
 struct __align__(128) DStage {
@@ -357,29 +367,32 @@ struct __align__(128) DStage {
 constexpr int kDStageBytes = sizeof(DStage);
 constexpr int kDThreads = kThreads + 32;
 
-struct DRunPlan {
-  int nruns;
-  int run_start[kMaxSegments + 1];
-  int64_t tiles_per_run[kMaxSegments];
+// Work is handed out dynamically in chunks of kDChunk tiles of one segment
+// (an atomic counter, claimed one chunk ahead by the producer): HBM bandwidth
+// is not shared evenly between SMs, and with static runs the CTAs finished
+// between 79 and 150 us of a 150 us launch (scripts/exp/timeline.py).
+struct DChunkPlan {
+  int64_t chunk_start[kMaxSegments + 1];            // prefix of per-segment chunk counts
 };
 
 __device__ __forceinline__ uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
-__global__ void __launch_bounds__(kDThreads)
-decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restrict__ out,
-                   int32_t* __restrict__ err, int write_out) {
+__global__ void __launch_bounds__(kDThreads, ZC_DMINB)   // CTAs / SM (register cap)
+decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restrict__ out,
+                   int32_t* __restrict__ err, unsigned* __restrict__ counter, int write_out) {
   extern __shared__ __align__(128) uint8_t s_dyn[];
   DStage* ring = reinterpret_cast<DStage*>(s_dyn);
   uint64_t* full = reinterpret_cast<uint64_t*>(s_dyn + kDStages * kDStageBytes);
   uint64_t* empty = full + kDStages;
   __shared__ __align__(16) uint32_t s_warp[2][kWarps];
-  __shared__ HeaderInfo s_hdr;
-  __shared__ int64_t s_lo[kDStages], s_al[kDStages], s_cnt[kDStages];
-  __shared__ int32_t s_gi_shift[kDStages];
+  __shared__ HeaderInfo s_hdr[kMaxSegments];
+  __shared__ int64_t s_lo[kDStages], s_al[kDStages], s_cnt[kDStages], s_tile[kDStages];
+  __shared__ int32_t s_gi_shift[kDStages], s_seg[kDStages];
   __shared__ uint32_t s_spread[256];
   __shared__ __align__(16) uint8_t s_slot[kThreads * kEPT];
 
   const int tid = threadIdx.x;
+  ZC_TL(0, 0);
   if (tid >= 32) {
     const int v = tid - 32;   // byte -> nibble spread: bit k -> bit 4k
     uint32_t sp = 0;
@@ -387,18 +400,12 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     for (int k = 0; k < 8; ++k) sp |= ((uint32_t(v) >> k) & 1u) << (4 * k);
     s_spread[v] = sp;
   }
-  // ---- this CTA's run ------------------------------------------------------
-  int seg = 0;
-  while (seg + 1 < segs.nseg && (int)blockIdx.x >= rp.run_start[seg + 1]) ++seg;
-  const int64_t seg_tiles = segs.tile_start[seg + 1] - segs.tile_start[seg];
-  int64_t t_begin = (blockIdx.x - rp.run_start[seg]) * rp.tiles_per_run[seg];
-  int64_t t_end = t_begin + rp.tiles_per_run[seg];
-  if (t_begin > seg_tiles) t_begin = seg_tiles;
-  if (t_end > seg_tiles) t_end = seg_tiles;
-  const uint8_t* frame = segs.stat[seg];
-
+  if (tid < segs.nseg) {   // every segment's header, validated once per CTA
+    const HeaderInfo h = check_header(segs.stat[tid], segs.n[tid], segs.dyn_len[tid]);
+    s_hdr[tid] = h;
+    if (h.err != kOk && blockIdx.x == 0) atomicMin(err + tid, h.err);
+  }
   if (tid == 0) {
-    s_hdr = check_header(frame, segs.n[seg], segs.dyn_len[seg]);
     for (int i = 0; i < kDStages; ++i) {
       mbar_init(full + i, 1);
       mbar_init(empty + i, kWarps);
@@ -406,79 +413,94 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     fence_mbar_init();
   }
   __syncthreads();
-  const HeaderInfo H = s_hdr;
-  if (H.err != kOk) {
-    if (tid == 0) atomicMin(err + seg, H.err);
-    return;
-  }
-  const int64_t n = H.n;
-  const int gsl = H.gsl;
-  const Layout L = layout_of(n, gsl);
-  const uint8_t* dyn = segs.dyn[seg] ? segs.dyn[seg] : frame + L.off[5];
-  const uint32_t* gi = reinterpret_cast<const uint32_t*>(frame + L.off[4]);
-  const int64_t gpt = int64_t(kTile) >> gsl;          // groups per full tile
-  const bool stage_gi = gsl >= 4;                     // slice fits kGiSlots
+  const int64_t nchunks = cp.chunk_start[segs.nseg];
 
   if (tid < 32) {
     // ======================= producer warp ===============================
     const int lane = tid;
-    const int64_t zcap = pad128(H.zc);
-    // escape-range bounds of 32 tiles at once: bound(t) = gi[first group of
-    // t]; the next chunk's bounds are loaded one chunk ahead, so the ring
-    // never drains behind a dependent global load
-    auto bound_of = [&](int64_t tb) -> uint32_t {
-      return tb < seg_tiles ? gi[tb * gpt] : (uint32_t)H.zc;
-    };
-    uint32_t bnd_next = bound_of(t_begin + lane);
-    for (int64_t c0 = t_begin; c0 < t_end; c0 += 32) {
-      const int64_t bnd = bnd_next;
-      bnd_next = bound_of(c0 + 32 + lane);
-      for (int j = 0; j < 32 && c0 + j < t_end; ++j) {
-        const int64_t lo = __shfl_sync(0xffffffffu, bnd, j);
-        const int64_t hi = (j < 31) ? __shfl_sync(0xffffffffu, bnd, j + 1)
-                                    : (int64_t)__shfl_sync(0xffffffffu, bnd_next, 0);
-        if (lane == 0) {
-          const int64_t t = c0 + j, k = t - t_begin;
-          const int st = (int)(k % kDStages);
-          if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
-          DStage& S = ring[st];
-          const int64_t e0 = t * kTile;
-          const int64_t valid = (n - e0) < kTile ? (n - e0) : kTile;
-          const uint32_t b_sm = r16(valid), b_pl = r16((valid + 7) >> 3);
-          // escapes: clamp into the section so a corrupt index stays memory-safe
-          int64_t clo = lo < 0 ? 0 : (lo > H.zc ? H.zc : lo);
-          int64_t chi = hi < clo ? clo : (hi > H.zc ? H.zc : hi);
-          const uint8_t* esrc = dyn + clo;
-          const uint8_t* eal = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(esrc) & ~uintptr_t(15));
-          int64_t eb = (int64_t)r16((uint64_t)(chi - clo) + (uint64_t)(esrc - eal));
-          if (eb > kEscSlots) eb = kEscSlots;
-          if ((eal - dyn) + eb > zcap + 128) eb = 0;   // never read past the padded section
-          // group_index slice [g0, g0 + ng] (+1 for the next tile's first entry)
-          uint32_t b_gi = 0;
-          const uint32_t* gsrc = gi;
-          int32_t shift = 0;
-          if (stage_gi) {
-            const int64_t g0 = t * gpt;
-            int64_t ng = (valid + (int64_t(1) << gsl) - 1) >> gsl;
-            if (g0 + ng < L.groups) ng += 1;
-            const uint32_t* gp = gi + g0;
-            gsrc = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
-            shift = (int32_t)(gp - gsrc);
-            b_gi = r16((uint64_t)(ng + shift) * 4);
+    int64_t k = 0;                                   // stages issued
+    unsigned cl = 0;
+    if (lane == 0) cl = atomicAdd(counter, 1u);
+    int64_t c = (int64_t)__shfl_sync(0xffffffffu, cl, 0);
+    while (c < nchunks) {
+      unsigned nx = 0;
+      if (lane == 0) nx = atomicAdd(counter, 1u);    // next claim overlaps this chunk
+      int seg = 0;
+      while (seg + 1 < segs.nseg && c >= cp.chunk_start[seg + 1]) ++seg;
+      const HeaderInfo H = s_hdr[seg];
+      if (H.err == kOk) {
+        const int64_t n = H.n;
+        const int gsl = H.gsl;
+        const Layout L = layout_of(n, gsl);
+        const uint8_t* frame = segs.stat[seg];
+        const uint8_t* dyn = segs.dyn[seg] ? segs.dyn[seg] : frame + L.off[5];
+        const uint32_t* gi = reinterpret_cast<const uint32_t*>(frame + L.off[4]);
+        const int64_t gpt = int64_t(kTile) >> gsl;
+        const bool stage_gi = gsl >= 4;              // slice fits kGiSlots
+        const int64_t seg_tiles = segs.tile_start[seg + 1] - segs.tile_start[seg];
+        const int64_t zcap = pad128(H.zc);
+        const int64_t t0 = (c - cp.chunk_start[seg]) * kDChunk;
+        const int64_t t1 = (t0 + kDChunk < seg_tiles) ? t0 + kDChunk : seg_tiles;
+        // escape-range bounds of the chunk's tiles: bound(t) = gi[first group of t]
+        const int64_t tb = t0 + lane;
+        uint32_t bnd = 0;
+        if (lane <= t1 - t0) bnd = tb < seg_tiles ? gi[tb * gpt] : (uint32_t)H.zc;
+        for (int64_t t = t0; t < t1; ++t) {
+          const int j = (int)(t - t0);
+          const int64_t lo = __shfl_sync(0xffffffffu, bnd, j);
+          const int64_t hi = __shfl_sync(0xffffffffu, bnd, j + 1);
+          if (lane == 0) {
+            const int st = (int)(k % kDStages);
+            if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
+            DStage& S = ring[st];
+            const int64_t e0 = t * kTile;
+            const int64_t valid = (n - e0) < kTile ? (n - e0) : kTile;
+            const uint32_t b_sm = r16(valid), b_pl = r16((valid + 7) >> 3);
+            // escapes: clamp into the section so a corrupt index stays memory-safe
+            int64_t clo = lo < 0 ? 0 : (lo > H.zc ? H.zc : lo);
+            int64_t chi = hi < clo ? clo : (hi > H.zc ? H.zc : hi);
+            const uint8_t* esrc = dyn + clo;
+            const uint8_t* eal = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(esrc) & ~uintptr_t(15));
+            int64_t eb = (int64_t)r16((uint64_t)(chi - clo) + (uint64_t)(esrc - eal));
+            if (eb > kEscSlots) eb = kEscSlots;
+            if ((eal - dyn) + eb > zcap + 128) eb = 0;   // never read past the padded section
+            // group_index slice [g0, g0 + ng] (+1 for the next tile's first entry)
+            uint32_t b_gi = 0;
+            const uint32_t* gsrc = gi;
+            int32_t shift = 0;
+            if (stage_gi) {
+              const int64_t g0 = t * gpt;
+              int64_t ng = (valid + (int64_t(1) << gsl) - 1) >> gsl;
+              if (g0 + ng < L.groups) ng += 1;
+              const uint32_t* gp = gi + g0;
+              gsrc = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
+              shift = (int32_t)(gp - gsrc);
+              b_gi = r16((uint64_t)(ng + shift) * 4);
+            }
+            s_lo[st] = clo;
+            s_al[st] = eal - dyn;
+            s_cnt[st] = chi - clo;
+            s_gi_shift[st] = shift;
+            s_tile[st] = t;
+            s_seg[st] = seg;
+            mbar_arrive_expect_tx(full + st, b_sm + 3 * b_pl + b_gi + (uint32_t)eb);
+            tma_load_1d(S.sm, frame + L.off[0] + e0, b_sm, full + st);
+            for (int b = 0; b < 3; ++b)
+              tma_load_1d(S.pl[b], frame + L.off[1 + b] + (e0 >> 3), b_pl, full + st);
+            if (b_gi) tma_load_1d(S.gi, gsrc, b_gi, full + st);
+            if (eb) tma_load_1d(S.esc, eal, (uint32_t)eb, full + st);
           }
-          s_lo[st] = clo;
-          s_al[st] = eal - dyn;
-          s_cnt[st] = chi - clo;
-          s_gi_shift[st] = shift;
-          mbar_arrive_expect_tx(full + st, b_sm + 3 * b_pl + b_gi + (uint32_t)eb);
-          tma_load_1d(S.sm, frame + L.off[0] + e0, b_sm, full + st);
-          for (int b = 0; b < 3; ++b)
-            tma_load_1d(S.pl[b], frame + L.off[1 + b] + (e0 >> 3), b_pl, full + st);
-          if (b_gi) tma_load_1d(S.gi, gsrc, b_gi, full + st);
-          if (eb) tma_load_1d(S.esc, eal, (uint32_t)eb, full + st);
+          __syncwarp();   // reconverge before the next shuffle (no BRA.DIV slow path)
+          ++k;
         }
-        __syncwarp();   // reconverge before the next shuffle (no BRA.DIV slow path)
       }
+      c = (int64_t)__shfl_sync(0xffffffffu, nx, 0);
+    }
+    if (lane == 0) {                                 // end marker for the consumers
+      const int st = (int)(k % kDStages);
+      if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
+      s_tile[st] = -1;
+      mbar_arrive(full + st);
     }
     return;
   }
@@ -488,110 +510,111 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
   // base is gi[first group of the warp] — warps are independent, no block
   // scan.  Mode B (1024 <= gs <= 4096): groups span warps; block scan.
   const int ct = tid - 32, lane = ct & 31, warp = ct >> 5;
-  const bool modeA = gsl <= 9;
-  const bool gs512 = gsl == 9;
   uint8_t* slot = s_slot + ct * kEPT;
-  uint16_t* const out_seg = out + segs.out_off[seg];
-  int32_t my_err = kOk;
-  // tiles [t_begin, t_fast_end) are full and take the lean gs = 512 path
-  const int64_t t_fast_end = gs512 ? (n / kTile < t_end ? n / kTile : t_end) : t_begin;
-  const bool out_aligned = ((reinterpret_cast<uintptr_t>(out_seg) & 15) == 0) && write_out;
-  const bool out_a32 = ((reinterpret_cast<uintptr_t>(out_seg) & 31) == 0) && write_out;
-  const int nfast = (int)(t_fast_end > t_begin ? t_fast_end - t_begin : 0);
-  const uint32_t zc32 = (uint32_t)H.zc;
-  const uint32_t ngroups32 = (uint32_t)L.groups;
-  const uint32_t g_begin = (uint32_t)(t_begin * gpt);
-  for (int k = 0; k < nfast; ++k) {
-    // ---------------- lean path: gs = 512, all 16 elements valid -----------
-    const int st = k & (kDStages - 1);
-    mbar_wait_warp(full + st, (uint32_t)((k / kDStages) & 1));
-    const DStage& S = ring[st];
-    const uint4 sv = *reinterpret_cast<const uint4*>(S.sm + ct * kEPT);
-#ifdef ZC_EXP_RING_ONLY
-    {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + st);
-      uint16_t* dst = out_seg + ((t_begin + k) * kTile + ct * kEPT);
-#if defined(ZC_EXP_NOSTORE)
-      if (sv.x == 0x9E3779B9u && sv.y == 0x7F4A7C15u) *dst = 1;
-#elif defined(ZC_EXP_PLAINSTORE)
-      *reinterpret_cast<uint4*>(dst) = sv;
-      *reinterpret_cast<uint4*>(dst + 8) = sv;
-#else
-      st_stream_v4(dst, sv);
-      st_stream_v4(dst + 8, sv);
-#endif
-      continue;
-    }
-#endif
-    const uint32_t p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + ct * 2);
-    const uint32_t p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + ct * 2);
-    const uint32_t p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
-    const uint32_t esc = ~(p0 | p1 | p2) & 0xFFFFu;
-    const uint32_t cnt = __popc(esc);
-    uint32_t incl = warp_incl_scan(cnt);
-    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-    const int gshift = s_gi_shift[st];
-    const uint32_t lo32 = (uint32_t)s_lo[st];
-    const int32_t tcnt = (int32_t)s_cnt[st];
-    const int32_t esc_off = (int32_t)(s_lo[st] - s_al[st]);
-    const uint32_t gwv = S.gi[gshift + warp];
-    const int32_t rank0 = (int32_t)(gwv - lo32 + incl - cnt);
-    if (lane == 0) {
-      const uint32_t g = g_begin + (uint32_t)k * 8u + (uint32_t)warp;
-      const bool has_next = g + 1 < ngroups32;
-      const uint32_t next = has_next ? S.gi[gshift + warp + 1] : zc32;
-      if (g == 0 && gwv != 0) my_err = kErrGroupIndex;
-      if (gwv + wtot != next) my_err = has_next ? kErrGroupIndex : kErrZeroCount;
-    }
-    const uint32_t lo8 = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
-    const uint32_t hi8 = s_spread[p0 >> 8] | s_spread[p1 >> 8] << 1 | s_spread[p2 >> 8] << 2;
-    uint32_t E0 = prmt(H.tbl_lo, H.tbl_hi, lo8);
-    uint32_t E1 = prmt(H.tbl_lo, H.tbl_hi, lo8 >> 16);
-    uint32_t E2 = prmt(H.tbl_lo, H.tbl_hi, hi8);
-    uint32_t E3 = prmt(H.tbl_lo, H.tbl_hi, hi8 >> 16);
-    if (esc) {
-      if (rank0 < 0 || rank0 + (int32_t)cnt > tcnt) {
-        my_err = kErrZeroCount;     // accompanied by a failing index check
-      } else {
-        *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
-        const uint8_t* eb = S.esc + esc_off + rank0;
-        uint32_t m = esc;
-        while (m) {
-          const int j = __ffs(m) - 1;
-          m &= m - 1;
-          slot[j] = *eb++;
-        }
-        const uint4 d = *reinterpret_cast<const uint4*>(slot);
-        E0 |= d.x; E1 |= d.y; E2 |= d.z; E3 |= d.w;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);
-    uint32_t o0, o1, o2, o3, o4, o5, o6, o7;
-    reassemble4(sv.x, E0, o0, o1);
-    reassemble4(sv.y, E1, o2, o3);
-    reassemble4(sv.z, E2, o4, o5);
-    reassemble4(sv.w, E3, o6, o7);
-    uint16_t* dst = out_seg + ((t_begin + k) * kTile + ct * kEPT);
-    if (out_a32) {
-      st_v8(dst, make_uint4(o0, o1, o2, o3), make_uint4(o4, o5, o6, o7));
-    } else if (out_aligned) {
-      st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
-      st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
-    } else if (write_out) {
-      const uint32_t ow[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
-#pragma unroll
-      for (int j = 0; j < kEPT; ++j) dst[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
-    }
-  }
-  for (int64_t t = t_begin + nfast; t < t_end; ++t) {
-    // ---------------- general path ---------------------------------------
-    const int64_t k = t - t_begin;
+  // per-segment state, reloaded when the stage's segment changes (uniform)
+  int cseg = -1;
+  uint32_t tbl_lo = 0, tbl_hi = 0;
+  int64_t zc = 0, groups = 0;
+  const uint32_t* gi = nullptr;
+  uint16_t* out_seg = out;
+  int64_t n = 0, gpt = 0;
+  int gsl = 0;
+  bool stage_gi = false, modeA = false, gs512 = false, out_aligned = false, out_a32 = false;
+  for (int64_t k = 0;; ++k) {
     const int st = (int)(k % kDStages);
     mbar_wait_warp(full + st, (uint32_t)((k / kDStages) & 1));
+    const int64_t t = s_tile[st];
+    if (t < 0) break;
+    const int seg = s_seg[st];
+    if (seg != cseg) {                               // uniform across the CTA
+      cseg = seg;
+      const HeaderInfo& H = s_hdr[seg];
+      n = H.n;
+      gsl = H.gsl;
+      zc = H.zc;
+      tbl_lo = H.tbl_lo;
+      tbl_hi = H.tbl_hi;
+      const Layout L = layout_of(n, gsl);
+      groups = L.groups;
+      gi = reinterpret_cast<const uint32_t*>(segs.stat[seg] + L.off[4]);
+      gpt = int64_t(kTile) >> gsl;
+      stage_gi = gsl >= 4;
+      modeA = gsl <= 9;
+      gs512 = gsl == 9;
+      out_seg = out + segs.out_off[seg];
+      out_aligned = ((reinterpret_cast<uintptr_t>(out_seg) & 15) == 0) && write_out;
+      out_a32 = ((reinterpret_cast<uintptr_t>(out_seg) & 31) == 0) && write_out;
+    }
     const DStage& S = ring[st];
     const int64_t tile_base = t * kTile;
+    int32_t my_err = kOk;
+    if (gs512 && tile_base + kTile <= n) {
+      // ---------------- lean path: gs = 512, all 16 elements valid -----------
+      const uint4 sv = *reinterpret_cast<const uint4*>(S.sm + ct * kEPT);
+      const uint32_t p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + ct * 2);
+      const uint32_t p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + ct * 2);
+      const uint32_t p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
+      const uint32_t esc = ~(p0 | p1 | p2) & 0xFFFFu;
+      const uint32_t cnt = __popc(esc);
+      uint32_t incl = warp_incl_scan(cnt);
+      const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+      const int gshift = s_gi_shift[st];
+      const uint32_t lo32 = (uint32_t)s_lo[st];
+      const int32_t tcnt = (int32_t)s_cnt[st];
+      const int32_t esc_off = (int32_t)(s_lo[st] - s_al[st]);
+      const uint32_t gwv = S.gi[gshift + warp];
+      const int32_t rank0 = (int32_t)(gwv - lo32 + incl - cnt);
+      if (lane == 0) {
+        const int64_t g = t * 8 + warp;
+        const bool has_next = g + 1 < groups;
+        const uint32_t next = has_next ? S.gi[gshift + warp + 1] : (uint32_t)zc;
+        if (g == 0 && gwv != 0) my_err = kErrGroupIndex;
+        if (gwv + wtot != next) my_err = has_next ? kErrGroupIndex : kErrZeroCount;
+      }
+      const uint32_t lo8 = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
+      const uint32_t hi8 = s_spread[p0 >> 8] | s_spread[p1 >> 8] << 1 | s_spread[p2 >> 8] << 2;
+      uint32_t E0 = prmt(tbl_lo, tbl_hi, lo8);
+      uint32_t E1 = prmt(tbl_lo, tbl_hi, lo8 >> 16);
+      uint32_t E2 = prmt(tbl_lo, tbl_hi, hi8);
+      uint32_t E3 = prmt(tbl_lo, tbl_hi, hi8 >> 16);
+      if (esc) {
+        if (rank0 < 0 || rank0 + (int32_t)cnt > tcnt) {
+          my_err = kErrZeroCount;     // accompanied by a failing index check
+        } else {
+          *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
+          const uint8_t* eb = S.esc + esc_off + rank0;
+          uint32_t m = esc;
+          while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            slot[j] = *eb++;
+          }
+          const uint4 d = *reinterpret_cast<const uint4*>(slot);
+          E0 |= d.x; E1 |= d.y; E2 |= d.z; E3 |= d.w;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+      uint32_t o0, o1, o2, o3, o4, o5, o6, o7;
+      reassemble4(sv.x, E0, o0, o1);
+      reassemble4(sv.y, E1, o2, o3);
+      reassemble4(sv.z, E2, o4, o5);
+      reassemble4(sv.w, E3, o6, o7);
+      uint16_t* dst = out_seg + (tile_base + ct * kEPT);
+      if (out_a32) {
+        st_v8(dst, make_uint4(o0, o1, o2, o3), make_uint4(o4, o5, o6, o7));
+      } else if (out_aligned) {
+        st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
+        st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
+      } else if (write_out) {
+        const uint32_t ow[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
+#pragma unroll
+        for (int j = 0; j < kEPT; ++j) dst[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
+      }
+      if (my_err != kOk) atomicMin(err + seg, my_err);
+      continue;
+    }
+    // ---------------- general path ---------------------------------------
     const int64_t base = tile_base + (int64_t)ct * kEPT;
     const int64_t rem = n - tile_base;                       // >= 1
     const int rem32 = rem >= kTile ? kTile : (int)rem;
@@ -604,7 +627,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     const int gshift = s_gi_shift[st];
     const int64_t g0 = t * gpt;
     auto gi_at = [&](int64_t g) -> int64_t {   // g within this tile, or its first successor
-      if (g >= L.groups) return H.zc;
+      if (g >= groups) return zc;
       if (stage_gi) return (int64_t)S.gi[gshift + (int)(g - g0)];
       return (int64_t)gi[g];
     };
@@ -623,16 +646,16 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
     const uint32_t wexcl = incl - cnt;               // escapes in the warp before me
     int32_t rank0;                                   // tile-local rank of my first escape
     if (gs512) {
-      // fast path (collectives): one group per warp, 32-bit math, staged slice
+      // one group per warp, 32-bit math, staged slice
       const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
       const bool warp_live = warp < live_warps;
       const uint32_t gwv = warp_live ? S.gi[gshift + warp] : 0u;
       rank0 = (int32_t)(gwv - (uint32_t)lo + wexcl);
       if (lane == 0 && warp_live) {
         const int64_t g = g0 + warp;
-        const uint32_t next = (g + 1 < L.groups) ? S.gi[gshift + warp + 1] : (uint32_t)H.zc;
+        const uint32_t next = (g + 1 < groups) ? S.gi[gshift + warp + 1] : (uint32_t)zc;
         if (g == 0 && gwv != 0) my_err = kErrGroupIndex;
-        if (gwv + wtot != next) my_err = (g + 1 < L.groups) ? kErrGroupIndex : kErrZeroCount;
+        if (gwv + wtot != next) my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
       }
     } else if (modeA) {
       const int64_t gw = (tile_base + warp * 512) >> gsl;     // warp's first group
@@ -649,7 +672,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
             const int64_t gv = lo + rank0;           // == gi[g] when consistent
             if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
             if (gi_at(g) != gv || gv + c != gi_at(g + 1))
-              my_err = (g + 1 < L.groups) ? kErrGroupIndex : kErrZeroCount;
+              my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
           }
         } else {
           const int gs = 1 << gsl;
@@ -659,7 +682,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
             const int64_t c = __popc(esc & (((1u << gs) - 1u) << j));
             if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
             if (gi_at(g) != lo + r || lo + r + c != gi_at(g + 1))
-              my_err = (g + 1 < L.groups) ? kErrGroupIndex : kErrZeroCount;
+              my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
             r += (int32_t)c;
           }
         }
@@ -679,7 +702,7 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
       }
       const uint32_t agg = __shfl_sync(0xffffffffu, vi, kWarps - 1);
       if (ct == 0) {
-        if ((int32_t)agg != tcnt) my_err = (g0 + gpt < L.groups) ? kErrGroupIndex : kErrZeroCount;
+        if ((int32_t)agg != tcnt) my_err = (g0 + gpt < groups) ? kErrGroupIndex : kErrZeroCount;
       }
     }
 
@@ -689,10 +712,10 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
       const uint32_t lo8 = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
       const uint32_t hi8 = s_spread[(p0 >> 8) & 0xFF] | s_spread[(p1 >> 8) & 0xFF] << 1 |
                            s_spread[(p2 >> 8) & 0xFF] << 2;
-      E0 = prmt(H.tbl_lo, H.tbl_hi, lo8);
-      E1 = prmt(H.tbl_lo, H.tbl_hi, lo8 >> 16);
-      E2 = prmt(H.tbl_lo, H.tbl_hi, hi8);
-      E3 = prmt(H.tbl_lo, H.tbl_hi, hi8 >> 16);
+      E0 = prmt(tbl_lo, tbl_hi, lo8);
+      E1 = prmt(tbl_lo, tbl_hi, lo8 >> 16);
+      E2 = prmt(tbl_lo, tbl_hi, hi8);
+      E3 = prmt(tbl_lo, tbl_hi, hi8 >> 16);
     }
     // ---- escapes: staged bytes at their tile-local rank -> per-thread slot ---
     if (esc) {
@@ -736,8 +759,9 @@ decode_ring_kernel(const DecodeSegs segs, const DRunPlan rp, uint16_t* __restric
           if (j < nv) dst[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
       }
     }
+    if (my_err != kOk) atomicMin(err + seg, my_err);
   }
-  if (my_err != kOk) atomicMin(err + seg, my_err);
+  ZC_TL(1, 32);
 }
 
 static int grid_cap(const void* fn, int threads, size_t dyn) {
@@ -784,23 +808,22 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
       if (want > 0 && want < cap2) cap2 = want;
     }
   }
-  DRunPlan rp{};
-  int runs = 0;
+  DChunkPlan cp{};
   for (int s = 0; s < segs.nseg; ++s) {
     const int64_t tiles = segs.tile_start[s + 1] - segs.tile_start[s];
-    int64_t want = (tiles * cap2 + ntiles - 1) / ntiles;
-    if (want < 1) want = 1;
-    if (want > tiles) want = tiles;
-    rp.run_start[s] = runs;
-    rp.tiles_per_run[s] = (tiles + want - 1) / want;
-    runs += (int)((tiles + rp.tiles_per_run[s] - 1) / rp.tiles_per_run[s]);
+    cp.chunk_start[s + 1] = cp.chunk_start[s] + (tiles + kDChunk - 1) / kDChunk;
   }
-  rp.run_start[segs.nseg] = runs;
-  rp.nruns = runs;
+  const int64_t nchunks = cp.chunk_start[segs.nseg];
+  const unsigned grid = (unsigned)(nchunks < cap2 ? nchunks : cap2);
+  unsigned* counter = reinterpret_cast<unsigned*>(ws);
+  e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
   prof_mark(kProfDecode, false, st);
-  decode_ring_kernel<<<runs, kDThreads, dyn, st>>>(segs, rp, out, err, write_out);
+  decode_ring_kernel<<<grid, kDThreads, dyn, st>>>(segs, cp, out, err, counter, write_out);
   prof_mark(kProfDecode, true, st);
   return cudaGetLastError();
 }
 
 }  // namespace zc
+
+ZC_TL_EXPORT(zc_debug_timeline_dec)

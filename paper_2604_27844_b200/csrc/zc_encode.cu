@@ -340,6 +340,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     for (int i = 0; i < 7; ++i) same = same && (book[i] == skip_if_same[i]);
     if (same) return;
   }
+  ZC_TL(2, 0);
   extern __shared__ __align__(128) uint8_t s_dyn[];
   uint8_t* ring = s_dyn;                                              // kStages x 8 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kStages * kStageBytes);
@@ -594,6 +595,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       encode_issue(xs, n, t + kStages, ring + st * kStageBytes, bars + st);
     }
   }
+  ZC_TL(5, 0);
   if (tid == 0) run_total[blockIdx.x] = run;
   if (run_status == nullptr) return;
 
@@ -645,6 +647,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       certify_block(spec.parts, gridDim.x, spec.total, spec.book, spec.result, spec.need);
     }
   }
+  ZC_TL(4, 0);
 }
 
 // Single-pass look-back path below this many tiles (latency wins), the
@@ -825,3 +828,5 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
 }
 
 }  // namespace zc
+
+ZC_TL_EXPORT(zc_debug_timeline_enc)
