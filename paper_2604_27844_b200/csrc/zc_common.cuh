@@ -214,6 +214,7 @@ constexpr uint64_t kValMask = (uint64_t(1) << 62) - 1;
 // earlier (atomic tile counter), so waiting cannot deadlock.
 constexpr int kLookbackPerLane = 8;
 
+template <int V = kLookbackPerLane>
 __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t tile,
                                                   int64_t chain_first, uint64_t agg,
                                                   uint64_t seed) {
@@ -227,22 +228,22 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t tile
   int64_t p = tile - 1;   // newest predecessor not yet accounted for
   while (true) {
     // lane l covers predecessors p - l*V - v, v = 0..V-1 (newest first)
-    uint64_t s[kLookbackPerLane];
+    uint64_t s[V];
 #pragma unroll
-    for (int v = 0; v < kLookbackPerLane; ++v) {
-      const int64_t q = p - (int64_t)lane * kLookbackPerLane - v;
+    for (int v = 0; v < V; ++v) {
+      const int64_t q = p - (int64_t)lane * V - v;
       s[v] = (q >= chain_first) ? ld_relaxed_u64(status + q) : kFlagInc;
     }
 #pragma unroll
-    for (int v = 0; v < kLookbackPerLane; ++v) {
-      const int64_t q = p - (int64_t)lane * kLookbackPerLane - v;
+    for (int v = 0; v < V; ++v) {
+      const int64_t q = p - (int64_t)lane * V - v;
       while ((s[v] >> 62) == 0) s[v] = ld_relaxed_u64(status + q);
     }
     // per lane: sum up to and including its newest inclusive entry
     uint64_t part = 0;
     bool hit = false;
 #pragma unroll
-    for (int v = 0; v < kLookbackPerLane; ++v) {
+    for (int v = 0; v < V; ++v) {
       if (!hit) {
         part += s[v] & kValMask;   // out-of-chain slots carry value 0
         hit = (s[v] & kFlagInc) != 0;
@@ -255,9 +256,72 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t tile
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     excl += v;
     if (inc_mask) break;
-    p -= 32 * kLookbackPerLane;
+    p -= 32 * V;
   }
   if (lane == 0) st_relaxed_u64(status + tile, kFlagInc | ((excl + agg) & kValMask));
+  return excl;
+}
+
+// CTA-wide variant for the run-level look-back of the encoder's epilogue
+// (every warp is idle there): warp w inspects the 256 predecessors
+// [p - 256 w - 255, p - 256 w] in the same round trip, so 2048 runs are
+// covered per L2 round trip without more registers per lane.  All threads
+// of the CTA call it; returns the exclusive prefix of `idx`.
+__device__ __forceinline__ uint64_t lookback_block(uint64_t* status, int64_t idx,
+                                                   int64_t chain_first, uint64_t agg) {
+  constexpr int V = kLookbackPerLane;
+  __shared__ uint64_t s_part[kWarps];
+  __shared__ int s_hit[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (idx == chain_first) {
+    if (tid == 0) st_relaxed_u64(status + idx, kFlagInc | (agg & kValMask));
+    return 0;
+  }
+  if (tid == 0) st_relaxed_u64(status + idx, kFlagAgg | (agg & kValMask));
+  uint64_t excl = 0;
+  int64_t p = idx - 1;
+  while (true) {
+    const int64_t pw = p - (int64_t)warp * 32 * V;   // this warp's newest entry
+    uint64_t sv[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int64_t q = pw - (int64_t)lane * V - v;
+      sv[v] = (q >= chain_first) ? ld_relaxed_u64(status + q) : kFlagInc;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int64_t q = pw - (int64_t)lane * V - v;
+      while ((sv[v] >> 62) == 0) {   // back off: early runs poll for tens of us
+        __nanosleep(256);             // while the rest of the grid still streams
+        sv[v] = ld_relaxed_u64(status + q);
+      }
+    }
+    uint64_t part = 0;
+    bool hit = false;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (!hit) {
+        part += sv[v] & kValMask;   // out-of-chain slots carry value 0
+        hit = (sv[v] & kFlagInc) != 0;
+      }
+    }
+    const unsigned inc_mask = __ballot_sync(0xffffffffu, hit);
+    const int first = inc_mask ? __ffs(inc_mask) - 1 : 32;
+    uint64_t wsum = (lane <= first) ? part : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    if (lane == 0) { s_part[warp] = wsum; s_hit[warp] = inc_mask != 0; }
+    __syncthreads();
+    bool done = false;
+    for (int w = 0; w < kWarps; ++w) {   // nearest warps first, up to the first hit
+      excl += s_part[w];
+      if (s_hit[w]) { done = true; break; }
+    }
+    __syncthreads();
+    if (done) break;
+    p -= (int64_t)kWarps * 32 * V;
+  }
+  if (tid == 0) st_relaxed_u64(status + idx, kFlagInc | ((excl + agg) & kValMask));
   return excl;
 }
 

@@ -267,12 +267,11 @@ encode_lookback_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs,
 // with TMA bulk copies (cp.async.bulk + mbarrier complete_tx), so three tiles
 // per CTA are loading while one is encoded.  The CTA writes the sign-mantissa
 // and plane sections in place, group_index entries relative to its own run,
-// its escapes compacted into its scratch run, and its escape total.
-// Its epilogue resolves the run's escape offset with a one-shot decoupled
-// look-back over the runs of the segment (every CTA is resident and
-// publishes its total before waiting), adds the offset to the run's
+// its escapes compacted into its scratch run, and its escape total, and
+// exits: no CTA waits for another.  encode_runfix_kernel (one CTA per run)
+// then sums the earlier runs' totals, adds the offset to the run's
 // group_index entries, moves the run's escapes to their final place, and
-// the segment's last run writes header + pads -- no second kernel.
+// the segment's last run writes header + pads.
 // Extra traffic: 2 x zero_count bytes (the scratch round trip).
 // ============================================================================
 
@@ -330,8 +329,7 @@ __global__ void __launch_bounds__(kThreads)
 encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const RunPlan rp,
                     const uint8_t* __restrict__ book, uint8_t* __restrict__ frames,
                     uint8_t* __restrict__ scratch, uint64_t* __restrict__ run_total,
-                    const SpecOut spec, const uint8_t* __restrict__ skip_if_same,
-                    uint64_t* __restrict__ run_status, uint64_t* __restrict__ frame_len) {
+                    const SpecOut spec, const uint8_t* __restrict__ skip_if_same) {
   // conditional launch (speculative path): the exact codebook equals the
   // guess the frames were already encoded with -> nothing to do
   if (skip_if_same != nullptr) {
@@ -597,26 +595,103 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
   }
   ZC_TL(5, 0);
   if (tid == 0) run_total[blockIdx.x] = run;
-  if (run_status == nullptr) return;
-
-  // ---- fused fix-up: escape offset of this run by a one-shot look-back over
-  // the runs of the segment (all CTAs are resident, each publishes its total
-  // before waiting), then finalize group_index, place escapes, header ------
-  __shared__ uint64_t s_off;
-  if (warp == 0) {
-    const uint64_t ex = lookback_warp(run_status, blockIdx.x, rp.run_start[seg], run, 0);
-    if (lane == 0) s_off = ex;
+  if (kSums) {
+    sums_block_finish(s1, s2, spec.parts + blockIdx.x);
+    __shared__ bool s_last;
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(spec.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      certify_block(spec.parts, gridDim.x, spec.total, spec.book, spec.result, spec.need);
+    }
   }
+  ZC_TL(4, 0);
+}
+
+// Fix-up of the runs (a second kernel, one CTA per run: no CTA of pass 1
+// ever waits for another, so nothing depends on all of them being resident
+// -- NCCL kernels may share the SMs -- and early runs do not poll L2 while
+// the stragglers stream; the in-kernel look-back left a 10 us tail after the
+// last run).  The run's escape offset is the sum of the earlier runs' totals
+// of its segment (<= 4096 values, read in parallel); then group_index gets
+// the offset added, the escapes move from scratch to the frame, and the
+// segment's last run writes header + pads.
+__global__ void __launch_bounds__(kThreads)
+encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __restrict__ book,
+                     uint8_t* __restrict__ frames, const uint8_t* __restrict__ scratch,
+                     const uint64_t* __restrict__ run_total,
+                     const uint8_t* __restrict__ skip_if_same, uint64_t* __restrict__ frame_len) {
+  if (skip_if_same != nullptr) {   // same condition as the pass-1 launch it follows
+    bool same = true;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) same = same && (book[i] == skip_if_same[i]);
+    if (same) return;
+  }
+  __shared__ uint8_t s_book[8];
+  __shared__ uint64_t s_red[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int seg;
+  int64_t t_begin, t_end;
+  run_range(segs, rp, blockIdx.x, seg, t_begin, t_end);
+  if (tid < 7) s_book[tid] = book[tid];
+  const int gsl = segs.gs_log2;
+  const int64_t n = segs.n[seg];
+  const Layout L = layout_of(n, gsl);
+  uint8_t* frame = frames + segs.frame_off[seg];
+  uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
+  const uint8_t* esc_out = scratch + (segs.tile_start[seg] + t_begin) * kTile;   // 16-B aligned
+  const uint32_t run = (uint32_t)run_total[blockIdx.x];
+  const int64_t e0 = t_begin * kTile;
+  const int64_t e1 = (t_end * kTile < n) ? t_end * kTile : n;
+  const int64_t g0 = (e0 + (int64_t(1) << gsl) - 1) >> gsl;
+  const int64_t g1 = t_begin < t_end ? (e1 + (int64_t(1) << gsl) - 1) >> gsl : g0;
+  // loads that do not depend on the offset go first (one round trip for all)
+  constexpr int kGiPer = 4;
+  const bool gi_fast = g1 - g0 <= (int64_t)kGiPer * kThreads;
+  uint32_t gv[kGiPer];
+#pragma unroll
+  for (int k = 0; k < kGiPer; ++k) {
+    const int64_t g = g0 + tid + (int64_t)k * kThreads;
+    gv[k] = (gi_fast && g < g1) ? gi[g] : 0u;
+  }
+  const bool esc_fast = run <= 16u * kThreads;
+  uint4 ev = make_uint4(0, 0, 0, 0);
+  if (esc_fast && 16u * tid < run) ev = *reinterpret_cast<const uint4*>(esc_out + 16 * tid);
+  // offset: the earlier runs' totals of this segment
+  uint64_t acc = 0;
+  for (int r = rp.run_start[seg] + tid; r < (int)blockIdx.x; r += kThreads) acc += run_total[r];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) s_red[warp] = acc;
   __syncthreads();
-  const uint64_t P = s_off;
-  if (t_begin < t_end) {
-    const int64_t e0 = t_begin * kTile;
-    const int64_t e1 = (t_end * kTile < n) ? t_end * kTile : n;
-    const int64_t g0 = (e0 + (int64_t(1) << gsl) - 1) >> gsl;
-    const int64_t g1 = (e1 + (int64_t(1) << gsl) - 1) >> gsl;
-    if (P != 0)
-      for (int64_t g = g0 + tid; g < g1; g += kThreads) gi[g] += (uint32_t)P;
-    uint8_t* dst = frame + L.off[5] + P;
+  uint64_t P = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) P += s_red[w];
+  // group_index += P
+  if (gi_fast) {
+#pragma unroll
+    for (int k = 0; k < kGiPer; ++k) {
+      const int64_t g = g0 + tid + (int64_t)k * kThreads;
+      if (g < g1 && P != 0) gi[g] = gv[k] + (uint32_t)P;
+    }
+  } else if (P != 0) {
+    for (int64_t g = g0 + tid; g < g1; g += kThreads) gi[g] += (uint32_t)P;
+  }
+  // escapes -> frame + off5 + P
+  uint8_t* dst = frame + L.off[5] + P;
+  if (esc_fast) {
+    const uint32_t b0 = 16u * tid;
+    if (b0 < run) {
+      const uint32_t wv[4] = {ev.x, ev.y, ev.z, ev.w};
+      const uint32_t lim = run - b0 < 16u ? run - b0 : 16u;
+#pragma unroll
+      for (uint32_t j = 0; j < 16; ++j)
+        if (j < lim) dst[b0 + j] = (uint8_t)(wv[j >> 2] >> (8 * (j & 3)));
+    }
+  } else {
     const uint32_t head = (uint32_t)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
     const uint32_t h = run < head ? run : head;
     if (tid < h) dst[tid] = esc_out[tid];
@@ -633,21 +708,6 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     write_header_and_pads(frame, L, zc, s_book);
     if (tid == 0) frame_len[seg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
   }
-  if (kSums) {
-    // after the fix-up, so the certificate never delays a run's look-back
-    sums_block_finish(s1, s2, spec.parts + blockIdx.x);
-    __shared__ bool s_last;
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(spec.done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      certify_block(spec.parts, gridDim.x, spec.total, spec.book, spec.result, spec.need);
-    }
-  }
-  ZC_TL(4, 0);
 }
 
 // Single-pass look-back path below this many tiles (latency wins), the
@@ -703,39 +763,26 @@ static int tiles_cap() {
   return cap1;
 }
 
-// pass 1 with the fused fix-up epilogue (run-level look-back); optional fused
-// certificate (spec) / conditional execution (skip_if_same) for the
-// speculative path.  run_status: nruns zeroed words (zeroed here unless the
-// caller already did).
+// pass 1 + run fix-up; optional fused certificate (spec) / conditional
+// execution (skip_if_same) for the speculative path.  Nothing to zero.
 static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, const RunPlan& rp,
                                    const uint8_t* book, uint8_t* frames, uint8_t* w8,
                                    uint64_t* frame_len, const SpecOut* spec,
-                                   const uint8_t* skip_if_same, uint64_t* run_status,
-                                   bool zero_status, cudaStream_t st) {
+                                   const uint8_t* skip_if_same, cudaStream_t st) {
   uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
   uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea;
-  if (zero_status) {
-    cudaError_t e = cudaMemsetAsync(run_status, 0, 8 * (size_t)rp.nruns, st);
-    if (e != cudaSuccess) return e;
-  }
   const bool timed = skip_if_same == nullptr;   // not the conditional re-encode
   if (timed) prof_mark(kProfEncode, false, st);
   if (spec)
     encode_tiles_kernel<true><<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
-        x, segs, rp, book, frames, scratch, run_total, *spec, skip_if_same, run_status,
-        frame_len);
+        x, segs, rp, book, frames, scratch, run_total, *spec, skip_if_same);
   else
     encode_tiles_kernel<false><<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
-        x, segs, rp, book, frames, scratch, run_total, SpecOut{}, skip_if_same, run_status,
-        frame_len);
+        x, segs, rp, book, frames, scratch, run_total, SpecOut{}, skip_if_same);
+  encode_runfix_kernel<<<rp.nruns, kThreads, 0, st>>>(segs, rp, book, frames, scratch, run_total,
+                                                      skip_if_same, frame_len);
   if (timed) prof_mark(kProfEncode, true, st);
   return cudaGetLastError();
-}
-
-// run-level look-back words of the default path: the last 32 KB of the
-// speculative area (4096 runs max)
-static uint64_t* default_run_status(uint8_t* w8) {
-  return reinterpret_cast<uint64_t*>(w8 + 256 + 8 * 4096 + kSpecArea - 8 * 4096);
 }
 
 cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8_t* book,
@@ -756,8 +803,7 @@ cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8
   }
   const RunPlan rp = make_plan(segs, tiles_cap());
   if (rp.nruns > 4096) return cudaErrorInvalidValue;
-  return launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, nullptr,
-                         default_run_status(w8), true, st);
+  return launch_two_pass(x, segs, rp, book, frames, w8, frame_len, nullptr, nullptr, st);
 }
 
 cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
@@ -803,7 +849,6 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   //   [192K, 320K)   exact-pass partials (32 B per CTA)
   //   [320K]         guess book; [320K+64] need flag
   //   [448K-64, 448K) counters: guess, certificate, exact pass
-  //   [448K, 480K)   run status of the re-encode; [480K, 512K) of the encode
   uint8_t* spec = w8 + 256 + 8 * 4096;
   SumPartial* guess_parts = reinterpret_cast<SumPartial*>(spec);
   SumPartial* run_sums = reinterpret_cast<SumPartial*>(spec + 128 * 1024);
@@ -811,20 +856,16 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   uint8_t* guess = spec + 320 * 1024;
   int* need = reinterpret_cast<int*>(spec + 320 * 1024 + 64);
   unsigned* counters = reinterpret_cast<unsigned*>(spec + 448 * 1024 - 64);
-  uint64_t* status2 = reinterpret_cast<uint64_t*>(spec + 448 * 1024);
-  uint64_t* status1 = default_run_status(w8);
-  // one memset: counters + both status arrays (contiguous)
-  cudaError_t e = cudaMemsetAsync(counters, 0, 64 + 8 * 4096 + 8 * (size_t)rp.nruns, st);
+  cudaError_t e = cudaMemsetAsync(counters, 0, 64, st);
   if (e != cudaSuccess) return e;
   e = launch_guess(x, ss, guess_parts, counters + 0, guess, st);
   if (e != cudaSuccess) return e;
   const SpecOut so{run_sums, counters + 1, total, book, result, need};
-  e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, &so, nullptr, status1, false, st);
+  e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, &so, nullptr, st);
   if (e != cudaSuccess) return e;
   e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms, st);
   if (e != cudaSuccess) return e;
-  return launch_two_pass(x, segs, rp2, book, frames, w8, frame_len, nullptr, guess, status2, false,
-                         st);
+  return launch_two_pass(x, segs, rp2, book, frames, w8, frame_len, nullptr, guess, st);
 }
 
 }  // namespace zc

@@ -31,6 +31,7 @@ lib.zc_debug_timeline_enc.argtypes = [ctypes.c_void_p]
 assert lib.zc_debug_timeline_dec(buf.ctypes.data) == 0
 assert lib.zc_debug_timeline_enc(enc.ctypes.data) == 0
 buf[2:6] = enc[2:6]
+encx = enc
 res = {}
 for name, a, b in (("decode", 0, 1), ("encode_pass1", 2, 5), ("encode_total", 2, 4)):
     st, en = buf[a].astype(np.int64), buf[b].astype(np.int64)
@@ -44,4 +45,22 @@ for name, a, b in (("decode", 0, 1), ("encode_pass1", 2, 5), ("encode_total", 2,
                  "end_p50_us": float(np.percentile(en - t0, 50) / 1e3),
                  "end_max_us": float((en.max() - t0) / 1e3),
                  "dur_min_us": float(d.min()), "dur_max_us": float(d.max())}
+t0e = enc[2][enc[2] > 0].astype(np.int64).min()
+for name, slot in (("enc_after_lookback", 0), ("enc_after_fixup", 1)):
+    v = enc[slot][enc[slot] > 0].astype(np.int64) - t0e
+    res[name] = {"min_us": float(v.min() / 1e3), "p50_us": float(np.percentile(v, 50) / 1e3),
+                 "max_us": float(v.max() / 1e3)}
+p1 = enc[5].astype(np.int64) - t0e
+lb = enc[0].astype(np.int64) - t0e
+ok = (enc[5] > 0) & (enc[0] > 0)
+idx = np.nonzero(ok)[0]
+strag = idx[np.argmax(p1[idx])]
+res["straggler"] = {"cta": int(strag), "pass1_end_us": float(p1[strag] / 1e3),
+                    "lookback_end_us": float(lb[strag] / 1e3)}
+top = idx[np.argsort(-lb[idx])[:6]]
+res["latest_lookbacks"] = [(int(i), round(float(p1[i] / 1e3), 1), round(float(lb[i] / 1e3), 1))
+                           for i in top]
+late = idx[np.argsort(-p1[idx])[:8]]
+res["latest_pass1"] = [(int(i), round(float(p1[i] / 1e3), 1), round(float(lb[i] / 1e3), 1))
+                       for i in late]
 print(json.dumps(res, indent=1))
