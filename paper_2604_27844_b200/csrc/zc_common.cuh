@@ -262,69 +262,6 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t tile
   return excl;
 }
 
-// CTA-wide variant for the run-level look-back of the encoder's epilogue
-// (every warp is idle there): warp w inspects the 256 predecessors
-// [p - 256 w - 255, p - 256 w] in the same round trip, so 2048 runs are
-// covered per L2 round trip without more registers per lane.  All threads
-// of the CTA call it; returns the exclusive prefix of `idx`.
-__device__ __forceinline__ uint64_t lookback_block(uint64_t* status, int64_t idx,
-                                                   int64_t chain_first, uint64_t agg) {
-  constexpr int V = kLookbackPerLane;
-  __shared__ uint64_t s_part[kWarps];
-  __shared__ int s_hit[kWarps];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (idx == chain_first) {
-    if (tid == 0) st_relaxed_u64(status + idx, kFlagInc | (agg & kValMask));
-    return 0;
-  }
-  if (tid == 0) st_relaxed_u64(status + idx, kFlagAgg | (agg & kValMask));
-  uint64_t excl = 0;
-  int64_t p = idx - 1;
-  while (true) {
-    const int64_t pw = p - (int64_t)warp * 32 * V;   // this warp's newest entry
-    uint64_t sv[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int64_t q = pw - (int64_t)lane * V - v;
-      sv[v] = (q >= chain_first) ? ld_relaxed_u64(status + q) : kFlagInc;
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int64_t q = pw - (int64_t)lane * V - v;
-      while ((sv[v] >> 62) == 0) {   // back off: early runs poll for tens of us
-        __nanosleep(256);             // while the rest of the grid still streams
-        sv[v] = ld_relaxed_u64(status + q);
-      }
-    }
-    uint64_t part = 0;
-    bool hit = false;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      if (!hit) {
-        part += sv[v] & kValMask;   // out-of-chain slots carry value 0
-        hit = (sv[v] & kFlagInc) != 0;
-      }
-    }
-    const unsigned inc_mask = __ballot_sync(0xffffffffu, hit);
-    const int first = inc_mask ? __ffs(inc_mask) - 1 : 32;
-    uint64_t wsum = (lane <= first) ? part : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-    if (lane == 0) { s_part[warp] = wsum; s_hit[warp] = inc_mask != 0; }
-    __syncthreads();
-    bool done = false;
-    for (int w = 0; w < kWarps; ++w) {   // nearest warps first, up to the first hit
-      excl += s_part[w];
-      if (s_hit[w]) { done = true; break; }
-    }
-    __syncthreads();
-    if (done) break;
-    p -= (int64_t)kWarps * 32 * V;
-  }
-  if (tid == 0) st_relaxed_u64(status + idx, kFlagInc | ((excl + agg) & kValMask));
-  return excl;
-}
-
 // Segment tables passed by value (A2A per-peer batching).
 struct EncodeSegs {
   int nseg;

@@ -87,7 +87,7 @@ if __name__ == "__main__":
     PROF.mkdir(exist_ok=True)
     launches(tag)
     traffic = {}
-    for k in ("decode_ring", "encode_tiles", "guess_kernel"):
+    for k in ("decode_ring", "encode_tiles", "encode_runfix", "guess_kernel"):
         b, t = kernel_summary(tag, k)
         traffic[f"{k if k.endswith('kernel') else k + '_kernel'}_per_launch_bytes"] = b
     traffic["source"] = f"ncu --set full captures prof_bench_{tag}_*.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum)"
