@@ -440,6 +440,38 @@ def run_ours(args):
                 "encode_leg_note": "codebook_for+compress: guess kernel (1/128 sample), encoder "
                                    "pass 1 with the statistic fused + run fix-up, three "
                                    "conditional launches"}
+    else:
+        # this rank's encoder (HBM-bound: its 2n-byte shard in, F-byte frame
+        # out) over eager zip_all_gather steps with the library's event hooks;
+        # the decoder reads W-1 peer frames (over NVLink on the peer-memory
+        # data plane), so it is reported beside, not as the HBM roofline
+        frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device=dev)
+        _, _, fl = engine.encode_measured(words, [(0, n)], 9, frames, [0])
+        F = int(fl.item())
+        frame_bytes = F
+        del frames
+        engine.profile_enable(True)
+        for _ in range(args.steps):
+            coll.zip_all_gather(comm, shard)
+        torch.cuda.synchronize()
+        engine.profile_enable(False)
+        enc_k = engine.profile_read(engine.PROF_ENCODE)
+        dec_k = engine.profile_read(engine.PROF_DECODE)
+        peak, peak_kind = measured_peak_hbm()
+        alg = 2 * n + F
+        k_ms = sum(enc_k) / len(enc_k)
+        ach = alg / (k_ms / 1e3) / 1e9
+        dec_ms = sum(dec_k) / len(dec_k) if dec_k else None
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None,
+                "kernel": "encode_tiles_kernel+encode_runfix_kernel", "peak_kind": peak_kind,
+                "alg_bytes_per_launch": alg, "kernel_ms": k_ms,
+                "timing": f"rank 0, CUDA events around the encoder launches of {args.steps} "
+                          "eager zip_all_gather steps after the timed region",
+                "decode_ring_kernel": {
+                    "ms": dec_ms, "bytes_per_launch": (world - 1) * (F + 2 * n),
+                    "GBps": ((world - 1) * (F + 2 * n) / (dec_ms / 1e3) / 1e9) if dec_ms else None,
+                    "note": "batched decode of the W-1 peer frames"}}
 
     # ---- end to end through the public API (host buffers) --------------------
     e2e = None
@@ -489,6 +521,36 @@ def run_ours(args):
                "note": "H2D of the shard from pinned memory + codebook_for + compress + "
                        "decompress through the public API; reads back sigma-derived book, "
                        "frame length/zero_count and the decoder's error word"}
+
+    elif world > 1:
+        # every rank: H2D of its shard from pinned memory + zip_all_gather
+        # through the public API (which reads back the decoders' error words
+        # and, on the NCCL data plane, the frame lengths); max over ranks
+        host = shard.cpu().pin_memory()
+        e_steps = max(2, min(args.steps, 5))
+
+        def api_step():
+            return coll.zip_all_gather(comm, host.to(dev, non_blocking=True))
+        res = None
+        for _ in range(max(3, args.warmup)):
+            res = None
+            res = api_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ts = time.perf_counter()
+        for _ in range(e_steps):
+            res = None
+            res = api_step()
+        torch.cuda.synchronize()
+        el = torch.tensor([(time.perf_counter() - ts) * 1e3 / e_steps], device=dev)
+        del res
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e_ms = float(el.item())
+        d2h = 4 * (world - 1) + (4 if comm.use_p2p else 8 * world)
+        e2e = {"value": total_bytes / (e_ms / 1e3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
+               "note": "per rank: H2D of the shard from pinned memory + zip_all_gather through "
+                       "the public API; wall clock, max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
