@@ -124,6 +124,17 @@ int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64
               const int64_t* n, const int64_t* out_off, int nseg, uint16_t* out,
               int32_t* err_dev, void* ws, int64_t ws_bytes, int write_out, void* stream);
 
+/* Replaces codec.decompress_group (codec.py:330-348), generalised to a
+ * range: the words of groups [g0, g1) of a frame of n elements with group
+ * size 1 << gs_log2 are written to out[0 ..), reading only those groups'
+ * sign-mantissa / plane bytes and their escapes (from group_index[g0]).
+ * The frame's structure must have been validated (zc_decode with
+ * write_out = 0, as the reference validates first); escape positions are
+ * clamped, so a corrupt frame cannot cause out-of-bounds reads.  frame is
+ * 8-byte aligned. */
+int zc_decode_groups(const uint8_t* frame, int64_t n, int gs_log2, int64_t g0, int64_t g1,
+                     uint16_t* out, void* stream);
+
 /* ---- peer memory for the compressed collectives over NVLink -------------
  * Replace the transport seam (transport.Communicator send/recv,
  * transport.py:559-623) for the pull-decode all-gather / all-to-all:

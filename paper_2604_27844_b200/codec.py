@@ -478,10 +478,12 @@ def decompress(chunk: CompressedChunk, out: torch.Tensor | None = None) -> torch
 
 
 def decompress_group(chunk: CompressedChunk, group: int) -> torch.Tensor:
-    """Words of one group (codec.py:330-348)."""
+    """Words of one group (codec.py:330-348): the chunk is validated first,
+    as in the reference, then only the group's bytes and its escapes (from
+    group_index[group]) are decoded on the device."""
     chunk.validate()
     n, gs = chunk.element_count, chunk.group_size
     n_groups = (n + gs - 1) // gs
     if not 0 <= group < n_groups:
         raise IndexError(f"group {group} out of range for {n_groups} groups")
-    return decompress(chunk)[group * gs:min(group * gs + gs, n)]
+    return engine.decode_groups(chunk.frame, n, gs.bit_length() - 1, group, group + 1)

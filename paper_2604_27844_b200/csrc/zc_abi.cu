@@ -14,6 +14,8 @@ cudaError_t launch_codebook_modal(const uint16_t*, const StatSegs&, int64_t, voi
 cudaError_t launch_encode(const uint16_t*, const EncodeSegs&, const uint8_t*, uint8_t*, void*,
                           uint64_t*, cudaStream_t);
 cudaError_t launch_decode(const DecodeSegs&, uint16_t*, int32_t*, void*, int, cudaStream_t);
+cudaError_t launch_decode_groups(const uint8_t*, int64_t, int, int64_t, int64_t, uint16_t*,
+                                 cudaStream_t);
 int64_t encode_workspace_bytes(int64_t ntiles);
 cudaError_t launch_encode_auto(const uint16_t*, const EncodeSegs&, const StatSegs&, int64_t,
                                uint8_t*, void*, uint64_t*, uint8_t*, double*, int, cudaStream_t);
@@ -239,6 +241,15 @@ int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64
   }
   if (128 + 8 * s.tile_start[nseg] > ws_bytes) return kStatusWorkspace;
   return status_of(launch_decode(s, out, err_dev, ws, write_out, stream));  // write_out: flags
+}
+
+int zc_decode_groups(const uint8_t* frame, int64_t n, int gs_log2, int64_t g0, int64_t g1,
+                     uint16_t* out, cudaStream_t stream) {
+  if (!frame || !out || n < 1 || gs_log2 < 0 || gs_log2 > 30) return kStatusBadArg;
+  if ((reinterpret_cast<uintptr_t>(frame) & 7) != 0) return kStatusBadArg;
+  const int64_t groups = (n + (int64_t(1) << gs_log2) - 1) >> gs_log2;
+  if (g0 < 0 || g1 < g0 || g1 > groups) return kStatusBadArg;
+  return status_of(launch_decode_groups(frame, n, gs_log2, g0, g1, out, stream));
 }
 
 }  // extern "C"

@@ -824,6 +824,93 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
   return cudaGetLastError();
 }
 
+
+
+
+// ============================================================================
+// Group random access (reference codec.decompress_group, codec.py:330-348):
+// decode groups [g0, g1) of a frame whose structure was validated, reading
+// only those groups' sign-mantissa / plane bytes and their escapes, which
+// start at group_index[g] -- no earlier escape data is touched.  One CTA per
+// group (grid-strided); a group is walked in 4096-element tiles with a block
+// scan carrying the escape rank.  Escape positions are clamped into the
+// section, so even an unvalidated frame stays memory-safe.
+// ============================================================================
+__global__ void __launch_bounds__(kThreads)
+decode_groups_kernel(const uint8_t* __restrict__ frame, int64_t n, int gsl, int64_t g0,
+                     int64_t g1, uint16_t* __restrict__ out) {
+  __shared__ uint32_t s_warp[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Layout L = layout_of(n, gsl);
+  const uint64_t zc = reinterpret_cast<const uint64_t*>(frame)[2];
+  const uint8_t* e8 = reinterpret_cast<const uint8_t*>(frame) + 24;   // entries[0..6]
+  const uint8_t* sm = frame + L.off[0];
+  const uint8_t* pl0 = frame + L.off[1];
+  const uint8_t* pl1 = frame + L.off[2];
+  const uint8_t* pl2 = frame + L.off[3];
+  const uint32_t* gi = reinterpret_cast<const uint32_t*>(frame + L.off[4]);
+  const uint8_t* dyn = frame + L.off[5];
+  const int64_t gs = int64_t(1) << gsl;
+  for (int64_t g = g0 + blockIdx.x; g < g1; g += gridDim.x) {
+    const int64_t s = g * gs;
+    const int64_t e = (s + gs < n) ? s + gs : n;
+    uint64_t run = gi[g];
+    for (int64_t tb = s; tb < e; tb += kTile) {
+      const int64_t base = tb + (int64_t)tid * kEPT;
+      uint32_t esc = 0, code[kEPT];
+#pragma unroll
+      for (int j = 0; j < kEPT; ++j) {
+        const int64_t k = base + j;
+        uint32_t c = 0;
+        if (k < e) {
+          const int sh = (int)(k & 7);
+          c = ((pl0[k >> 3] >> sh) & 1u) | ((pl1[k >> 3] >> sh) & 1u) << 1 |
+              ((pl2[k >> 3] >> sh) & 1u) << 2;
+          if (c == 0) esc |= 1u << j;
+        }
+        code[j] = c;
+      }
+      const uint32_t cnt = __popc(esc);
+      const uint32_t incl = warp_incl_scan(cnt);
+      if (lane == 31) s_warp[warp] = incl;
+      __syncthreads();
+      uint32_t wbase = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        wbase += (w < warp) ? s_warp[w] : 0u;
+        tot += s_warp[w];
+      }
+      uint64_t pos = run + wbase + incl - cnt;
+#pragma unroll
+      for (int j = 0; j < kEPT; ++j) {
+        const int64_t k = base + j;
+        if (k < e) {
+          uint32_t ex;
+          if (code[j]) {
+            ex = e8[code[j] - 1];
+          } else {
+            ex = pos < zc ? dyn[pos] : 0u;
+            ++pos;
+          }
+          const uint32_t b = sm[k];
+          out[k - g0 * gs] = (uint16_t)(((b & 0x80u) << 8) | (ex << 7) | (b & 0x7Fu));
+        }
+      }
+      run += tot;
+      __syncthreads();   // s_warp reuse
+    }
+  }
+}
+
+cudaError_t launch_decode_groups(const uint8_t* frame, int64_t n, int gsl, int64_t g0, int64_t g1,
+                                 uint16_t* out, cudaStream_t st) {
+  if (g1 <= g0) return cudaSuccess;
+  const int64_t ng = g1 - g0;
+  const unsigned grid = (unsigned)(ng < 4096 ? ng : 4096);
+  decode_groups_kernel<<<grid, kThreads, 0, st>>>(frame, n, gsl, g0, g1, out);
+  return cudaGetLastError();
+}
+
 }  // namespace zc
 
 ZC_TL_EXPORT(zc_debug_timeline_dec)

@@ -185,6 +185,19 @@ def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_
     return err
 
 
+def decode_groups(frame: torch.Tensor, n: int, gs_log2: int, g0: int, g1: int,
+                  out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Words of groups [g0, g1) of a validated frame (zc_decode_groups)."""
+    gs = 1 << gs_log2
+    count = max(0, min(g1 * gs, n) - g0 * gs)
+    if out is None:
+        out = torch.empty(count, dtype=torch.int16, device=frame.device)
+    if count:
+        check(lib().zc_decode_groups(frame.data_ptr(), int(n), int(gs_log2), int(g0), int(g1),
+                                     out.data_ptr(), stream_ptr(stream)), "zc_decode_groups")
+    return out
+
+
 PROF_ENCODE, PROF_DECODE = 0, 1
 
 

@@ -183,6 +183,29 @@ def test_group_random_access():
         zc.decompress_group(zc.compress(gaussian_words(100), codec.derive_codebook(1.0)), 1)
 
 
+@pytest.mark.parametrize("n,gs,book", [(1000, 1, "gauss"), (1001, 2, "gauss"), (999, 8, "miss"),
+                                       (5000, 16, "gauss"), (9000, 4096, "miss"),
+                                       ((1 << 20) + 77, 1 << 20, "gauss"),
+                                       (300_000, 8192, "gauss")])
+def test_group_ranges_decode_only_those_groups(n, gs, book):
+    # zc_decode_groups over single groups and ranges, against the oracle's
+    # words; "miss" = a book no exponent hits (every element escapes)
+    data = gaussian_words(n, seed=gs)
+    cb = codec.derive_codebook(1.0) if book == "gauss" else codec.ExponentCodebook(
+        (10, 11, 12, 13, 14, 15, 16))
+    chunk = zc.compress(data, cb, group_size=gs)
+    chunk.validate()
+    ng = (n + gs - 1) // gs
+    rng = np.random.default_rng(n)
+    picks = sorted({0, ng - 1, *rng.integers(0, ng, size=min(ng, 6)).tolist()})
+    for g in picks:
+        got = host_words(engine.decode_groups(chunk.frame, n, gs.bit_length() - 1, g, g + 1))
+        assert np.array_equal(got, data[g * gs:(g + 1) * gs]), g
+    a, b = ng // 3, min(ng, ng // 3 + 5)
+    got = host_words(engine.decode_groups(chunk.frame, n, gs.bit_length() - 1, a, b))
+    assert np.array_equal(got, data[a * gs:min(b * gs, n)])
+
+
 def test_chunk_from_sections_validation():
     c = zc.compress(gaussian_words(2000, seed=42), codec.derive_codebook(1.0))
     sm, planes, gi, ze = c.sign_mantissa, c.exp_planes, c.group_index, c.zero_exponents
