@@ -143,6 +143,17 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   return v;
 }
 
+// Inclusive scan within each 16-lane half of a warp (segment mask 0x1000).
+__device__ __forceinline__ uint32_t half_incl_scan(uint32_t v) {
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1)
+    asm volatile("{ .reg .u32 t; .reg .pred p;\n\t"
+                 "shfl.sync.up.b32 t|p, %0, %1, 0x1000, -1;\n\t"
+                 "@p add.u32 %0, %0, t; }"
+                 : "+r"(v) : "r"(o));
+  return v;
+}
+
 // (a & m) | (b & ~m) as one LOP3
 __device__ __forceinline__ uint32_t bitsel(uint32_t m, uint32_t a, uint32_t b) {
   uint32_t d;

@@ -357,6 +357,8 @@ decode_lookback_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_
 constexpr int kDStages = ZC_DSTAGES;
 constexpr int kDChunk = ZC_DCHUNK;                  // tiles per dynamic claim
 constexpr int kGiSlots = 264;                       // up to 257 gi entries (gs >= 16) + align
+// Every escape byte of a tile is staged (a smaller slot with a global-memory
+// overflow path measured 4 % slower: the extra select alone cost registers).
 constexpr int kEscSlots = kTile + 32;
 struct __align__(128) DStage {
   uint8_t sm[kTile];
@@ -384,12 +386,12 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
   DStage* ring = reinterpret_cast<DStage*>(s_dyn);
   uint64_t* full = reinterpret_cast<uint64_t*>(s_dyn + kDStages * kDStageBytes);
   uint64_t* empty = full + kDStages;
-  __shared__ __align__(16) uint32_t s_warp[2][kWarps];
+  __shared__ __align__(16) uint32_t s_wsum[2][2][8];   // consumer group x parity x virtual warp
   __shared__ HeaderInfo s_hdr[kMaxSegments];
   __shared__ int64_t s_lo[kDStages], s_al[kDStages], s_cnt[kDStages], s_tile[kDStages];
   __shared__ int32_t s_gi_shift[kDStages], s_seg[kDStages];
   __shared__ uint32_t s_spread[256];
-  __shared__ __align__(16) uint8_t s_slot[kThreads * kEPT];
+  __shared__ __align__(16) uint8_t s_slot[kThreads * 32];
 
   const int tid = threadIdx.x;
   ZC_TL(0, 0);
@@ -408,7 +410,7 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
   if (tid == 0) {
     for (int i = 0; i < kDStages; ++i) {
       mbar_init(full + i, 1);
-      mbar_init(empty + i, kWarps);
+      mbar_init(empty + i, kWarps / 2);             // the 4 warps of one consumer group
     }
     fence_mbar_init();
   }
@@ -496,21 +498,32 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
       }
       c = (int64_t)__shfl_sync(0xffffffffu, nx, 0);
     }
-    if (lane == 0) {                                 // end marker for the consumers
-      const int st = (int)(k % kDStages);
-      if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
-      s_tile[st] = -1;
-      mbar_arrive(full + st);
+    if (lane == 0) {                  // end markers: one for each consumer group
+      for (int e = 0; e < 2; ++e, ++k) {
+        const int st = (int)(k % kDStages);
+        if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
+        s_tile[st] = -1;
+        mbar_arrive(full + st);
+      }
     }
     return;
   }
 
   // ========================= consumer warps ==============================
-  // Mode A (gs <= 512): a warp's 512 elements start a group, so its escape
-  // base is gi[first group of the warp] — warps are independent, no block
-  // scan.  Mode B (1024 <= gs <= 4096): groups span warps; block scan.
-  const int ct = tid - 32, lane = ct & 31, warp = ct >> 5;
-  uint8_t* slot = s_slot + ct * kEPT;
+  // Two groups of 4 warps take alternate stages (group g: k = 2i + g), so a
+  // tile is decoded by 128 threads.  Lean path (gs = 512, full tile): each
+  // lane owns 32 consecutive words -- half the per-word fixed cost of 16 --
+  // and each half-warp one 512-word group (segmented scan over 16 lanes).
+  // Other tiles: two passes of the 16-word logic over virtual threads
+  // vct = 128 p + ct (virtual warp vw = 4 p + warp covers 512 words).
+  // Mode A (gs <= 512): a virtual warp's 512 words start a group, so its
+  // escape base is gi[first group of the warp] — no group-wide scan.  Mode B
+  // (1024 <= gs <= 4096): groups span warps; one group-wide scan over the 8
+  // virtual warps of the tile (named barrier per consumer group).
+  const int ct0 = tid - 32;                          // 0..255
+  const int grp = ct0 >> 7;                          // consumer group
+  const int ct = ct0 & 127, lane = ct & 31, warp = ct >> 5;
+  uint8_t* slot = s_slot + ct0 * 32;                 // 32 B per thread
   // per-segment state, reloaded when the stage's segment changes (uniform)
   int cseg = -1;
   uint32_t tbl_lo = 0, tbl_hi = 0;
@@ -520,13 +533,14 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
   int64_t n = 0, gpt = 0;
   int gsl = 0;
   bool stage_gi = false, modeA = false, gs512 = false, out_aligned = false, out_a32 = false;
-  for (int64_t k = 0;; ++k) {
+  for (int64_t i = 0;; ++i) {
+    const int64_t k = 2 * i + grp;
     const int st = (int)(k % kDStages);
     mbar_wait_warp(full + st, (uint32_t)((k / kDStages) & 1));
     const int64_t t = s_tile[st];
     if (t < 0) break;
     const int seg = s_seg[st];
-    if (seg != cseg) {                               // uniform across the CTA
+    if (seg != cseg) {                               // uniform across the group
       cseg = seg;
       const HeaderInfo& H = s_hdr[seg];
       n = H.n;
@@ -547,216 +561,259 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
     }
     const DStage& S = ring[st];
     const int64_t tile_base = t * kTile;
+    const int64_t lo = s_lo[st];
+    const int32_t tcnt = (int32_t)s_cnt[st];
+    const int32_t esc_off = (int32_t)(lo - s_al[st]);
+    const int gshift = s_gi_shift[st];
+    const uint8_t* esc_base = S.esc + esc_off;   // this tile's staged escapes
     int32_t my_err = kOk;
     if (gs512 && tile_base + kTile <= n) {
-      // ---------------- lean path: gs = 512, all 16 elements valid -----------
-      const uint4 sv = *reinterpret_cast<const uint4*>(S.sm + ct * kEPT);
-      const uint32_t p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + ct * 2);
-      const uint32_t p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + ct * 2);
-      const uint32_t p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
-      const uint32_t esc = ~(p0 | p1 | p2) & 0xFFFFu;
+      // ---------------- lean path: gs = 512, full tile, 32 words / lane ------
+      const int half = lane >> 4;
+      const uint4 sa = *reinterpret_cast<const uint4*>(S.sm + ct * 32);
+      const uint4 sb = *reinterpret_cast<const uint4*>(S.sm + ct * 32 + 16);
+      const uint32_t p0 = *reinterpret_cast<const uint32_t*>(S.pl[0] + ct * 4);
+      const uint32_t p1 = *reinterpret_cast<const uint32_t*>(S.pl[1] + ct * 4);
+      const uint32_t p2 = *reinterpret_cast<const uint32_t*>(S.pl[2] + ct * 4);
+      const uint32_t esc = ~(p0 | p1 | p2);
       const uint32_t cnt = __popc(esc);
-      uint32_t incl = warp_incl_scan(cnt);
-      const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-      const int gshift = s_gi_shift[st];
-      const uint32_t lo32 = (uint32_t)s_lo[st];
-      const int32_t tcnt = (int32_t)s_cnt[st];
-      const int32_t esc_off = (int32_t)(s_lo[st] - s_al[st]);
-      const uint32_t gwv = S.gi[gshift + warp];
-      const int32_t rank0 = (int32_t)(gwv - lo32 + incl - cnt);
-      if (lane == 0) {
-        const int64_t g = t * 8 + warp;
+      const uint32_t incl = half_incl_scan(cnt);
+      const uint32_t htot = __shfl_sync(0xffffffffu, incl, lane | 15);
+      const int gl = 2 * warp + half;                // group within the tile
+      const uint32_t gwv = S.gi[gshift + gl];
+      const int32_t rank0 = (int32_t)(gwv - (uint32_t)lo + incl - cnt);
+      if ((lane & 15) == 0) {
+        const int64_t g = t * 8 + gl;
         const bool has_next = g + 1 < groups;
-        const uint32_t next = has_next ? S.gi[gshift + warp + 1] : (uint32_t)zc;
+        const uint32_t next = has_next ? S.gi[gshift + gl + 1] : (uint32_t)zc;
         if (g == 0 && gwv != 0) my_err = kErrGroupIndex;
-        if (gwv + wtot != next) my_err = has_next ? kErrGroupIndex : kErrZeroCount;
+        if (gwv + htot != next) my_err = has_next ? kErrGroupIndex : kErrZeroCount;
       }
-      const uint32_t lo8 = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
-      const uint32_t hi8 = s_spread[p0 >> 8] | s_spread[p1 >> 8] << 1 | s_spread[p2 >> 8] << 2;
-      uint32_t E0 = prmt(tbl_lo, tbl_hi, lo8);
-      uint32_t E1 = prmt(tbl_lo, tbl_hi, lo8 >> 16);
-      uint32_t E2 = prmt(tbl_lo, tbl_hi, hi8);
-      uint32_t E3 = prmt(tbl_lo, tbl_hi, hi8 >> 16);
+      uint32_t E[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {                  // plane byte q: words 8q .. 8q+7
+        const uint32_t sp = s_spread[(p0 >> (8 * q)) & 0xFF] |
+                            s_spread[(p1 >> (8 * q)) & 0xFF] << 1 |
+                            s_spread[(p2 >> (8 * q)) & 0xFF] << 2;
+        E[2 * q] = prmt(tbl_lo, tbl_hi, sp);
+        E[2 * q + 1] = prmt(tbl_lo, tbl_hi, sp >> 16);
+      }
       if (esc) {
         if (rank0 < 0 || rank0 + (int32_t)cnt > tcnt) {
           my_err = kErrZeroCount;     // accompanied by a failing index check
         } else {
           *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
-          const uint8_t* eb = S.esc + esc_off + rank0;
+          *reinterpret_cast<uint4*>(slot + 16) = make_uint4(0, 0, 0, 0);
+          const uint8_t* eb = esc_base + rank0;
           uint32_t m = esc;
           while (m) {
             const int j = __ffs(m) - 1;
             m &= m - 1;
             slot[j] = *eb++;
           }
-          const uint4 d = *reinterpret_cast<const uint4*>(slot);
-          E0 |= d.x; E1 |= d.y; E2 |= d.z; E3 |= d.w;
+          const uint4 d0 = *reinterpret_cast<const uint4*>(slot);
+          const uint4 d1 = *reinterpret_cast<const uint4*>(slot + 16);
+          E[0] |= d0.x; E[1] |= d0.y; E[2] |= d0.z; E[3] |= d0.w;
+          E[4] |= d1.x; E[5] |= d1.y; E[6] |= d1.z; E[7] |= d1.w;
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st);
-      uint32_t o0, o1, o2, o3, o4, o5, o6, o7;
-      reassemble4(sv.x, E0, o0, o1);
-      reassemble4(sv.y, E1, o2, o3);
-      reassemble4(sv.z, E2, o4, o5);
-      reassemble4(sv.w, E3, o6, o7);
-      uint16_t* dst = out_seg + (tile_base + ct * kEPT);
+      uint32_t o[16];
+      reassemble4(sa.x, E[0], o[0], o[1]);
+      reassemble4(sa.y, E[1], o[2], o[3]);
+      reassemble4(sa.z, E[2], o[4], o[5]);
+      reassemble4(sa.w, E[3], o[6], o[7]);
+      reassemble4(sb.x, E[4], o[8], o[9]);
+      reassemble4(sb.y, E[5], o[10], o[11]);
+      reassemble4(sb.z, E[6], o[12], o[13]);
+      reassemble4(sb.w, E[7], o[14], o[15]);
+      uint16_t* dst = out_seg + (tile_base + ct * 32);
       if (out_a32) {
-        st_v8(dst, make_uint4(o0, o1, o2, o3), make_uint4(o4, o5, o6, o7));
+        st_v8(dst, make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]));
+        st_v8(dst + 16, make_uint4(o[8], o[9], o[10], o[11]),
+              make_uint4(o[12], o[13], o[14], o[15]));
       } else if (out_aligned) {
-        st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
-        st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
-      } else if (write_out) {
-        const uint32_t ow[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
 #pragma unroll
-        for (int j = 0; j < kEPT; ++j) dst[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
+        for (int q = 0; q < 4; ++q)
+          st_stream_v4(dst + 8 * q, make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
+      } else if (write_out) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dst[j] = (uint16_t)(o[j >> 1] >> (16 * (j & 1)));
       }
       if (my_err != kOk) atomicMin(err + seg, my_err);
       continue;
     }
-    // ---------------- general path ---------------------------------------
-    const int64_t base = tile_base + (int64_t)ct * kEPT;
+    // ---------------- general path: two passes of 16 words / thread --------
     const int64_t rem = n - tile_base;                       // >= 1
     const int rem32 = rem >= kTile ? kTile : (int)rem;
-    const int nv = rem32 - ct * kEPT >= kEPT ? kEPT : rem32 - ct * kEPT;   // may be <= 0
     const int live_warps = (rem32 + 511) >> 9;
-    const uint32_t valid16 = nv >= kEPT ? 0xFFFFu : (nv > 0 ? ((1u << nv) - 1u) : 0u);
-    const int64_t lo = s_lo[st];
-    const int32_t tcnt = (int32_t)s_cnt[st];
-    const int32_t esc_off = (int32_t)(lo - s_al[st]);
-    const int gshift = s_gi_shift[st];
     const int64_t g0 = t * gpt;
     auto gi_at = [&](int64_t g) -> int64_t {   // g within this tile, or its first successor
       if (g >= groups) return zc;
       if (stage_gi) return (int64_t)S.gi[gshift + (int)(g - g0)];
       return (int64_t)gi[g];
     };
-
-    uint4 sv = make_uint4(0, 0, 0, 0);
-    uint32_t p0 = 0, p1 = 0, p2 = 0;
-    if (nv > 0) {
-      sv = *reinterpret_cast<const uint4*>(S.sm + ct * kEPT);
-      p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + ct * 2);
-      p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + ct * 2);
-      p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + ct * 2);
-    }
-    const uint32_t esc = ~(p0 | p1 | p2) & valid16;
-    const uint32_t cnt = __popc(esc);
-    uint32_t incl = warp_incl_scan(cnt);
-    const uint32_t wexcl = incl - cnt;               // escapes in the warp before me
-    int32_t rank0;                                   // tile-local rank of my first escape
-    if (gs512) {
-      // one group per warp, 32-bit math, staged slice
-      const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-      const bool warp_live = warp < live_warps;
-      const uint32_t gwv = warp_live ? S.gi[gshift + warp] : 0u;
-      rank0 = (int32_t)(gwv - (uint32_t)lo + wexcl);
-      if (lane == 0 && warp_live) {
-        const int64_t g = g0 + warp;
-        const uint32_t next = (g + 1 < groups) ? S.gi[gshift + warp + 1] : (uint32_t)zc;
-        if (g == 0 && gwv != 0) my_err = kErrGroupIndex;
-        if (gwv + wtot != next) my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
-      }
-    } else if (modeA) {
-      const int64_t gw = (tile_base + warp * 512) >> gsl;     // warp's first group
-      const bool warp_live = tile_base + warp * 512 < n;
-      const int32_t wbase = warp_live ? (int32_t)(gi_at(gw) - lo) : 0;
-      rank0 = wbase + (int32_t)wexcl;
-      const int tpg = gsl >= 4 ? 1 << (gsl - 4) : 1;          // threads per group
-      const uint32_t gend = __shfl_sync(0xffffffffu, incl, (lane | (tpg - 1)) & 31);
+    uint4 sv[2];
+    uint32_t escv[2], cntv[2], inclv[2], spv[2][2];
+    int nvv[2];
+    int32_t rank0v[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int vct = 128 * p + ct;
+      const int nv = rem32 - vct * kEPT >= kEPT ? kEPT : rem32 - vct * kEPT;   // may be <= 0
+      const uint32_t valid16 = nv >= kEPT ? 0xFFFFu : (nv > 0 ? ((1u << nv) - 1u) : 0u);
+      uint32_t p0 = 0, p1 = 0, p2 = 0;
+      sv[p] = make_uint4(0, 0, 0, 0);
       if (nv > 0) {
-        if (gsl >= 4) {
-          if ((lane & (tpg - 1)) == 0) {
-            const int64_t g = base >> gsl;
-            const int64_t c = (int64_t)(gend - wexcl);
-            const int64_t gv = lo + rank0;           // == gi[g] when consistent
-            if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
-            if (gi_at(g) != gv || gv + c != gi_at(g + 1))
-              my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
+        sv[p] = *reinterpret_cast<const uint4*>(S.sm + vct * kEPT);
+        p0 = *reinterpret_cast<const uint16_t*>(S.pl[0] + vct * 2);
+        p1 = *reinterpret_cast<const uint16_t*>(S.pl[1] + vct * 2);
+        p2 = *reinterpret_cast<const uint16_t*>(S.pl[2] + vct * 2);
+      }
+      nvv[p] = nv;
+      escv[p] = ~(p0 | p1 | p2) & valid16;
+      cntv[p] = __popc(escv[p]);
+      inclv[p] = warp_incl_scan(cntv[p]);
+      spv[p][0] = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
+      spv[p][1] = s_spread[(p0 >> 8) & 0xFF] | s_spread[(p1 >> 8) & 0xFF] << 1 |
+                  s_spread[(p2 >> 8) & 0xFF] << 2;
+    }
+    if (modeA) {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int vw = 4 * p + warp, vct = 128 * p + ct;
+        const int64_t base = tile_base + (int64_t)vct * kEPT;
+        const int nv = nvv[p];
+        const uint32_t esc = escv[p], incl = inclv[p], wexcl = incl - cntv[p];
+        if (gs512) {
+          // one group per virtual warp, 32-bit math, staged slice
+          const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+          const bool warp_live = vw < live_warps;
+          const uint32_t gwv = warp_live ? S.gi[gshift + vw] : 0u;
+          rank0v[p] = (int32_t)(gwv - (uint32_t)lo + wexcl);
+          if (lane == 0 && warp_live) {
+            const int64_t g = g0 + vw;
+            const uint32_t next = (g + 1 < groups) ? S.gi[gshift + vw + 1] : (uint32_t)zc;
+            if (g == 0 && gwv != 0) my_err = kErrGroupIndex;
+            if (gwv + wtot != next) my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
           }
         } else {
-          const int gs = 1 << gsl;
-          int32_t r = rank0;
-          for (int j = 0; j < kEPT && j < nv; j += gs) {
-            const int64_t g = (base + j) >> gsl;
-            const int64_t c = __popc(esc & (((1u << gs) - 1u) << j));
-            if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
-            if (gi_at(g) != lo + r || lo + r + c != gi_at(g + 1))
-              my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
-            r += (int32_t)c;
+          const int64_t gw = (tile_base + vw * 512) >> gsl;     // warp's first group
+          const bool warp_live = tile_base + vw * 512 < n;
+          const int32_t wbase = warp_live ? (int32_t)(gi_at(gw) - lo) : 0;
+          const int32_t rank0 = wbase + (int32_t)wexcl;
+          rank0v[p] = rank0;
+          const int tpg = gsl >= 4 ? 1 << (gsl - 4) : 1;          // threads per group
+          const uint32_t gend = __shfl_sync(0xffffffffu, incl, (lane | (tpg - 1)) & 31);
+          if (nv > 0) {
+            if (gsl >= 4) {
+              if ((lane & (tpg - 1)) == 0) {
+                const int64_t g = base >> gsl;
+                const int64_t c = (int64_t)(gend - wexcl);
+                const int64_t gv = lo + rank0;           // == gi[g] when consistent
+                if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
+                if (gi_at(g) != gv || gv + c != gi_at(g + 1))
+                  my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
+              }
+            } else {
+              const int gs = 1 << gsl;
+              int32_t r = rank0;
+              for (int j = 0; j < kEPT && j < nv; j += gs) {
+                const int64_t g = (base + j) >> gsl;
+                const int64_t c = __popc(esc & (((1u << gs) - 1u) << j));
+                if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
+                if (gi_at(g) != lo + r || lo + r + c != gi_at(g + 1))
+                  my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
+                r += (int32_t)c;
+              }
+            }
           }
         }
       }
     } else {
-      uint32_t* sw = s_warp[k & 1];
-      if (lane == 31) sw[warp] = incl;
-      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
-      const uint32_t v = lane < kWarps ? sw[lane] : 0u;
-      const uint32_t vi = warp_incl_scan<kWarps>(v);
-      const uint32_t wb = __shfl_sync(0xffffffffu, vi - v, warp);
-      rank0 = (int32_t)(wb + wexcl);
-      if (nv > 0 && (base & ((int64_t(1) << gsl) - 1)) == 0) {
-        const int64_t g = base >> gsl;
-        if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
-        if (gi_at(g) != lo + rank0) my_err = kErrGroupIndex;
+      // mode B: group-wide scan of the 8 virtual warps' escape counts
+      uint32_t* sw = s_wsum[grp][i & 1];
+      if (lane == 31) {
+        sw[warp] = inclv[0];
+        sw[4 + warp] = inclv[1];
       }
-      const uint32_t agg = __shfl_sync(0xffffffffu, vi, kWarps - 1);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(128) : "memory");
+      const uint32_t v = lane < 8 ? sw[lane] : 0u;
+      const uint32_t vi = warp_incl_scan<8>(v);
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int vw = 4 * p + warp, vct = 128 * p + ct;
+        const int64_t base = tile_base + (int64_t)vct * kEPT;
+        const uint32_t wb = __shfl_sync(0xffffffffu, vi - v, vw);
+        rank0v[p] = (int32_t)(wb + inclv[p] - cntv[p]);
+        if (nvv[p] > 0 && (base & ((int64_t(1) << gsl) - 1)) == 0) {
+          const int64_t g = base >> gsl;
+          if (g == 0 && gi_at(0) != 0) my_err = kErrGroupIndex;
+          if (gi_at(g) != lo + rank0v[p]) my_err = kErrGroupIndex;
+        }
+      }
+      const uint32_t agg = __shfl_sync(0xffffffffu, vi, 7);
       if (ct == 0) {
         if ((int32_t)agg != tcnt) my_err = (g0 + gpt < groups) ? kErrGroupIndex : kErrZeroCount;
       }
     }
-
-    // ---- exponents: codes -> PRMT table lookup ------------------------------
-    uint32_t E0, E1, E2, E3;
-    {
-      const uint32_t lo8 = s_spread[p0 & 0xFF] | s_spread[p1 & 0xFF] << 1 | s_spread[p2 & 0xFF] << 2;
-      const uint32_t hi8 = s_spread[(p0 >> 8) & 0xFF] | s_spread[(p1 >> 8) & 0xFF] << 1 |
-                           s_spread[(p2 >> 8) & 0xFF] << 2;
-      E0 = prmt(tbl_lo, tbl_hi, lo8);
-      E1 = prmt(tbl_lo, tbl_hi, lo8 >> 16);
-      E2 = prmt(tbl_lo, tbl_hi, hi8);
-      E3 = prmt(tbl_lo, tbl_hi, hi8 >> 16);
-    }
-    // ---- escapes: staged bytes at their tile-local rank -> per-thread slot ---
-    if (esc) {
-      if (rank0 < 0 || rank0 + (int32_t)cnt > tcnt) {
-        // escapes out of the staged range: always accompanied by a failing
-        // index check, which carries the field the reference names
-        my_err = kErrZeroCount;
-      } else {
-        *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
-        const uint8_t* eb = S.esc + esc_off + rank0;
-        uint32_t m = esc;
-        while (m) {
-          const int j = __ffs(m) - 1;
-          m &= m - 1;
-          slot[j] = *eb++;
+    // ---- exponents + escapes (staged bytes at their tile-local rank) --------
+    uint32_t E[2][4];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      E[p][0] = prmt(tbl_lo, tbl_hi, spv[p][0]);
+      E[p][1] = prmt(tbl_lo, tbl_hi, spv[p][0] >> 16);
+      E[p][2] = prmt(tbl_lo, tbl_hi, spv[p][1]);
+      E[p][3] = prmt(tbl_lo, tbl_hi, spv[p][1] >> 16);
+      const uint32_t esc = escv[p];
+      if (esc) {
+        const int32_t rank0 = rank0v[p];
+        if (rank0 < 0 || rank0 + (int32_t)cntv[p] > tcnt) {
+          // escapes out of the staged range: always accompanied by a failing
+          // index check, which carries the field the reference names
+          my_err = kErrZeroCount;
+        } else {
+          uint8_t* sl = slot + 16 * p;
+          *reinterpret_cast<uint4*>(sl) = make_uint4(0, 0, 0, 0);
+          const uint8_t* eb = esc_base + rank0;
+          uint32_t m = esc;
+          while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            sl[j] = *eb++;
+          }
+          const uint4 d = *reinterpret_cast<const uint4*>(sl);
+          E[p][0] |= d.x; E[p][1] |= d.y; E[p][2] |= d.z; E[p][3] |= d.w;
         }
-        const uint4 d = *reinterpret_cast<const uint4*>(slot);
-        E0 |= d.x; E1 |= d.y; E2 |= d.z; E3 |= d.w;
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
 
     // ---- reassemble (codec.py:308-312) and store ---------------------------
-    if (write_out && nv > 0) {
-      uint32_t o0, o1, o2, o3, o4, o5, o6, o7;
-      reassemble4(sv.x, E0, o0, o1);
-      reassemble4(sv.y, E1, o2, o3);
-      reassemble4(sv.z, E2, o4, o5);
-      reassemble4(sv.w, E3, o6, o7);
-      uint16_t* dst = out_seg + base;
-      if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
-        st_v8(dst, make_uint4(o0, o1, o2, o3), make_uint4(o4, o5, o6, o7));
-      } else if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-        st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
-        st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
-      } else {
-        const uint32_t ow[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
 #pragma unroll
-        for (int j = 0; j < kEPT; ++j)
-          if (j < nv) dst[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
+    for (int p = 0; p < 2; ++p) {
+      const int nv = nvv[p];
+      if (write_out && nv > 0) {
+        const int64_t base = tile_base + (int64_t)(128 * p + ct) * kEPT;
+        uint32_t o0, o1, o2, o3, o4, o5, o6, o7;
+        reassemble4(sv[p].x, E[p][0], o0, o1);
+        reassemble4(sv[p].y, E[p][1], o2, o3);
+        reassemble4(sv[p].z, E[p][2], o4, o5);
+        reassemble4(sv[p].w, E[p][3], o6, o7);
+        uint16_t* dst = out_seg + base;
+        if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
+          st_v8(dst, make_uint4(o0, o1, o2, o3), make_uint4(o4, o5, o6, o7));
+        } else if (nv == kEPT && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          st_stream_v4(dst, make_uint4(o0, o1, o2, o3));
+          st_stream_v4(dst + 8, make_uint4(o4, o5, o6, o7));
+        } else {
+          const uint32_t ow[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
+#pragma unroll
+          for (int j = 0; j < kEPT; ++j)
+            if (j < nv) dst[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
+        }
       }
     }
     if (my_err != kOk) atomicMin(err + seg, my_err);
