@@ -275,7 +275,13 @@ encode_lookback_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs,
 // Extra traffic: 2 x zero_count bytes (the scratch round trip).
 // ============================================================================
 
-constexpr int kStages = 4;
+#ifndef ZC_ESTAGES
+#define ZC_ESTAGES 4
+#endif
+#ifndef ZC_EMINB
+#define ZC_EMINB 4
+#endif
+constexpr int kStages = ZC_ESTAGES;
 constexpr int kStageBytes = kTile * 2;
 
 struct RunPlan {                      // pass-1 CTA -> (segment, tile run)
@@ -325,7 +331,7 @@ struct SpecOut {
 // kSums: also accumulate the certified packed-fp32 statistic of x (the
 // speculative codebook path) and certify it at the end.
 template <bool kSums>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, ZC_EMINB)
 encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const RunPlan rp,
                     const uint8_t* __restrict__ book, uint8_t* __restrict__ frames,
                     uint8_t* __restrict__ scratch, uint64_t* __restrict__ run_total,
@@ -388,7 +394,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     uint32_t* gi_w = gi + ((t_begin * kTile + tid * kEPT) >> 9);
     const bool gi512 = gsl == 9;
     for (int k = 0; k < nfast; ++k) {
-      const int st = k & (kStages - 1);
+      const int st = (int)((unsigned)k % (unsigned)kStages);
       const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
       mbar_wait_warp(bars + st, (uint32_t)((k / kStages) & 1));
       const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
