@@ -710,6 +710,114 @@ def run_moe_a2a(args):
     dist.destroy_process_group()
 
 
+def run_sweep(args):
+    """BASELINE configs[4]: message sizes 64 KiB .. 1 GiB (per rank).
+
+    N=1: the compressed path's own cost per size (measured codebook +
+    encode + decode of one message, CUDA-graph replays) and the link
+    bandwidth below which compression pays (the adaptive switch's flip
+    point: codec time < bytes x (1 - 1/ratio) / link bandwidth).
+    N>1: zip_all_gather vs the plain NCCL all-gather per size, max over
+    ranks, plus the switcher's choice from a cost model fitted on the
+    smallest/largest sizes (switcher.fit_cost_model).
+    """
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    if args.share_gpu:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2604_27844_b200 import engine, switcher
+    if world > 1:
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
+        from paper_2604_27844_b200 import collectives as coll
+        comm = coll.Communicator.from_process_group()
+        comm.use_p2p = args.transport == "p2p" and _preflight_p2p(comm, coll, dev)
+    sizes = [(64 << 10) << k for k in range(15)]                # 64 KiB .. 1 GiB
+    rows = []
+    g = torch.Generator(device=dev).manual_seed(rank)
+    for nbytes in sizes:
+        n = nbytes // 2
+        x = (torch.randn(n, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+        w = engine.words_view(x)
+        reps = max(3, min(50, (64 << 20) // nbytes))
+        if world == 1:
+            frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device=dev)
+            out = torch.empty_like(w)
+            flen = torch.empty(1, dtype=torch.int64, device=dev)
+            err = torch.empty(1, dtype=torch.int32, device=dev)
+
+            def step():
+                engine.encode_measured(w, [(0, n)], 9, frames, [0], flen)
+                engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err)
+            step()
+            torch.cuda.synchronize()
+            assert int(err.item()) == engine.ERR_OK and torch.equal(out, w)
+            F = int(flen.item())
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                step()
+            for _ in range(3):
+                gr.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            for _ in range(reps):
+                gr.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / reps
+            ratio = 2 * n / F
+            saved = nbytes * (1 - 1 / ratio)
+            rows.append({"bytes": nbytes, "codec_ms": ms, "codec_GBps": nbytes / (ms / 1e3) / 1e9,
+                         "ratio": ratio,
+                         "pays_below_link_GBps": saved / (ms / 1e3) / 1e9 if saved > 0 else 0.0})
+        else:
+            def timed(fn):
+                for _ in range(2):
+                    fn()
+                torch.cuda.synchronize()
+                dist.barrier()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(reps):
+                    fn()
+                b.record()
+                torch.cuda.synchronize()
+                t = torch.tensor([a.elapsed_time(b) / reps], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                return float(t.item())
+            t_zip = timed(lambda: coll.zip_all_gather(comm, x))
+            t_raw = timed(lambda: coll.reference_all_gather(comm, x))
+            rows.append({"bytes": nbytes, "zip_ms": t_zip, "raw_ms": t_raw,
+                         "zip_GBps": world * nbytes / (t_zip / 1e3) / 1e9,
+                         "raw_GBps": world * nbytes / (t_raw / 1e3) / 1e9})
+        del x, w
+    line = {"metric": METRIC, "workload": "c5 message-size sweep 64 KiB .. 1 GiB per rank",
+            "n_gpus": world, "unit": "GB/s", "data": "synthetic N(0, 0.02^2) BF16",
+            "rows": rows}
+    if world > 1:
+        ds = [r["bytes"] for r in rows]
+        e = 1 / 1.4244          # frame / raw bytes of N(0, 0.02^2) BF16 (BASELINE.md section 2)
+        model = switcher.fit_cost_model(ds, [r["raw_ms"] for r in rows],
+                                        [r["zip_ms"] for r in rows], e=e)
+        line["cost_model"] = {"alpha_native_ms": model.alpha_rs, "beta_native_ms_per_B": model.beta_rs,
+                              "alpha_zipped_ms": model.alpha_a2a,
+                              "beta_zipped_ms_per_B": model.beta_a2a, "e": e}
+        for r in rows:
+            r["switcher"] = switcher.select(model, r["bytes"]).value
+            r["best"] = "zipped" if r["zip_ms"] < r["raw_ms"] else "native"
+        line["transport"] = "p2p" if comm.use_p2p else "nccl"
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -721,9 +829,10 @@ def main():
     ap.add_argument("--clock-settle", type=float, default=1.0)
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the N=1 step eagerly (default: CUDA graph replays)")
-    ap.add_argument("--workload", default="layer_ag", choices=["layer_ag", "moe_a2a", "grad_mix"],
+    ap.add_argument("--workload", default="layer_ag",
+                    choices=["layer_ag", "moe_a2a", "grad_mix", "sweep"],
                     help="layer_ag: the headline line (configs[1]); moe_a2a: configs[2]; "
-                         "grad_mix: configs[3]")
+                         "grad_mix: configs[3]; sweep: configs[4]")
     ap.add_argument("--tokens", type=int, default=4096, help="moe_a2a tokens per rank")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
@@ -740,6 +849,8 @@ def main():
         run_grad_mix(args)
     elif args.workload == "moe_a2a":
         run_moe_a2a(args)
+    elif args.workload == "sweep":
+        run_sweep(args)
     else:
         run_ours(args)
 

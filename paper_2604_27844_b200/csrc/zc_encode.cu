@@ -716,9 +716,13 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
   }
 }
 
-// Single-pass look-back path below this many tiles (latency wins), the
-// two-kernel path above it (bandwidth wins).
-constexpr int64_t kLookbackMaxTiles = 256;
+// Single-pass look-back path up to this many tiles, the two-kernel path
+// above it: measured per-call latency (bench.py --workload sweep) favours
+// the two-kernel path from 32 tiles (256 KiB) on.
+#ifndef ZC_LBMAX
+#define ZC_LBMAX 16
+#endif
+constexpr int64_t kLookbackMaxTiles = ZC_LBMAX;
 
 static int grid_for(const void* fn, int threads, size_t dyn_smem) {
   int dev = 0, sms = 0, occ = 0;
