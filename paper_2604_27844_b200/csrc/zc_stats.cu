@@ -30,13 +30,11 @@
 namespace zc {
 
 __device__ void finalize_block(const Partial* parts, int64_t nparts, int64_t total_words,
-                               uint8_t* book, double* result, const uint8_t* guess,
-                               int* mismatch);
+                               uint8_t* book, double* result);
 
-// Persistent: each CTA owns a contiguous run of tiles (every `stride`-th
-// tile of the concatenated segments: 1 for the exact statistic, >1 for the
-// sampled guess) and keeps a kSStages-deep ring of 8 KB tiles in flight with
-// TMA bulk copies; thread 0 issues, all threads accumulate.  The last CTA to
+// Persistent: each CTA owns a contiguous run of tiles of the concatenated
+// segments and keeps a kSStages-deep ring of 8 KB tiles in flight with TMA
+// bulk copies; thread 0 issues, all threads accumulate.  The last CTA to
 // finish merges every partial in a fixed order and derives the codebook.
 constexpr int kSStages = 4;
 constexpr int kSStageBytes = kTile * 2;
@@ -57,7 +55,7 @@ __device__ __forceinline__ void stats_issue(const uint16_t* x, const StatSegs& s
 }
 
 __global__ void __launch_bounds__(kThreads)
-stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t stride,
+stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs,
              Partial* __restrict__ out, unsigned* __restrict__ done, int64_t total_words,
              uint8_t* __restrict__ book, double* __restrict__ result,
              const int* __restrict__ need) {
@@ -68,22 +66,21 @@ stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t stride
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kSStages * kSStageBytes);
   const int tid = threadIdx.x;
   const int64_t ntiles = segs.tile_start[segs.nseg];
-  const int64_t nsample = (ntiles + stride - 1) / stride;        // tiles this launch reads
-  const int64_t per = (nsample + gridDim.x - 1) / gridDim.x;
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t i0 = blockIdx.x * per;
-  const int64_t i1 = (i0 + per < nsample) ? i0 + per : nsample;
+  const int64_t i1 = (i0 + per < ntiles) ? i0 + per : ntiles;
   if (tid == 0) {
     for (int k = 0; k < kSStages; ++k) mbar_init(bars + k, 1);
     fence_mbar_init();
     for (int k = 0; k < kSStages && i0 + k < i1; ++k)
-      stats_issue(x, segs, (i0 + k) * stride, ring + k * kSStageBytes, bars + k);
+      stats_issue(x, segs, i0 + k, ring + k * kSStageBytes, bars + k);
   }
   __syncthreads();
   StatAcc acc;
   for (int64_t i = i0; i < i1; ++i) {
     const int k = (int)(i - i0);
     const int st = k & (kSStages - 1);
-    const int64_t tile = i * stride;
+    const int64_t tile = i;
     const int sg = find_seg(segs.tile_start, segs.nseg, tile);
     const uint16_t* xs = x + segs.x_off[sg];
     const int64_t base = (tile - segs.tile_start[sg]) * kTile;
@@ -115,7 +112,7 @@ stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t stride
     __syncthreads();                                   // stage free
     if (tid == 0 && i + kSStages < i1) {
       fence_proxy_async();
-      stats_issue(x, segs, (i + kSStages) * stride, ring + st * kSStageBytes, bars + st);
+      stats_issue(x, segs, i + kSStages, ring + st * kSStageBytes, bars + st);
     }
   }
   stat_block_finish(acc, out + blockIdx.x);
@@ -129,7 +126,7 @@ stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t stride
   __syncthreads();
   if (s_last) {
     __threadfence();
-    finalize_block(out, gridDim.x, total_words, book, result, nullptr, nullptr);
+    finalize_block(out, gridDim.x, total_words, book, result);
   }
 }
 
@@ -149,17 +146,12 @@ static int stats_grid_cap() {
   return cap;
 }
 
-// Final reduction + derivation.  One CTA of 1024 threads; thread t merges a
-// fixed contiguous range, then a fixed binary tree.  result[0] = sigma
-// (NaN when no finite value), result[1] = finite count, result[2] = path
-// (1 analytic, 2 modal), book = 7 entries.
-// Fixed-order merge of `nparts` partials by one kThreads-thread CTA, then the
-// reference derivation.  result[0] = sigma (NaN when no finite value),
-// result[1] = finite count, result[2] = path (1 analytic, 2 modal).  When
-// `mismatch` is given, *mismatch = (book != guess).
+// Fixed-order merge of `nparts` partials by one kThreads-thread CTA (each
+// thread a contiguous range, then a fixed binary tree), then the reference
+// derivation.  result[0] = sigma (NaN when no finite value), result[1] =
+// finite count, result[2] = path (1 analytic, 2 modal), book = 7 entries.
 __device__ void finalize_block(const Partial* parts, int64_t nparts, int64_t total_words,
-                               uint8_t* book, double* result, const uint8_t* guess,
-                               int* mismatch) {
+                               uint8_t* book, double* result) {
   __shared__ double f_n[kWarps], f_m[kWarps], f_q[kWarps];
   __shared__ int f_e[kWarps];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -211,19 +203,13 @@ __device__ void finalize_block(const Partial* parts, int64_t nparts, int64_t tot
       write_window(book, all_zero_exp ? -6 : mode - 127 - 3);
       result[2] = 2.0;
     }
-    if (mismatch) {
-      int diff = 0;
-      for (int i = 0; i < 7; ++i) diff |= (book[i] != guess[i]);
-      *mismatch = diff;
-    }
   }
 }
 
 __global__ void __launch_bounds__(kThreads)
 finalize_kernel(const Partial* __restrict__ parts, int64_t nparts, int64_t total_words,
-                uint8_t* __restrict__ book, double* __restrict__ result,
-                const uint8_t* __restrict__ guess, int* __restrict__ mismatch) {
-  finalize_block(parts, nparts, total_words, book, result, guess, mismatch);
+                uint8_t* __restrict__ book, double* __restrict__ result) {
+  finalize_block(parts, nparts, total_words, book, result);
 }
 
 
@@ -389,9 +375,9 @@ cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, in
           x, segs, reinterpret_cast<SumPartial*>(parts), done_sums, total, book, result, need);
     }
     stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(
-        x, segs, 1, parts, done, total, book, result, exact ? nullptr : need);
+        x, segs, parts, done, total, book, result, exact ? nullptr : need);
   } else {
-    finalize_kernel<<<1, kThreads, 0, st>>>(parts, 0, total, book, result, nullptr, nullptr);
+    finalize_kernel<<<1, kThreads, 0, st>>>(parts, 0, total, book, result);
   }
   return cudaGetLastError();
 }
@@ -407,33 +393,7 @@ cudaError_t launch_codebook_modal(const uint16_t* x, const StatSegs& segs, int64
   return cudaGetLastError();
 }
 
-// Sampled guess for the speculative encoder: every `stride`-th tile.
-cudaError_t launch_codebook_sampled(const uint16_t* x, const StatSegs& segs, int64_t stride,
-                                    Partial* parts, uint8_t* book, double* result,
-                                    cudaStream_t st) {
-  const int64_t ntiles = segs.tile_start[segs.nseg];
-  const int64_t sampled = (ntiles + stride - 1) / stride;
-  const int cap = stats_grid_cap();
-  const int64_t grid = sampled < cap ? sampled : cap;
-  unsigned* done = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(parts) - 64);
-  cudaError_t e = cudaMemsetAsync(done, 0, sizeof(unsigned), st);
-  if (e != cudaSuccess) return e;
-  stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(x, segs, stride, parts, done, 0,
-                                                                    book, result, nullptr);
-  return cudaGetLastError();
-}
-
-// Exact codebook from per-CTA partials; flags a mismatch with `guess`.
-cudaError_t launch_finalize(const Partial* parts, int64_t nparts, int64_t total, uint8_t* book,
-                            double* result, const uint8_t* guess, int* mismatch,
-                            cudaStream_t st) {
-  finalize_kernel<<<1, kThreads, 0, st>>>(parts, nparts, total, book, result, guess, mismatch);
-  return cudaGetLastError();
-}
-
 // ---- speculative encoder support (launch_encode_auto) -------------------------
-// Guess: the analytic codebook of the packed-fp32 sums over every `stride`-th
-// tile.  No certificate -- a wrong guess only costs a re-encode.
 // Guess for the speculative encoder: the analytic codebook of packed-fp32
 // sums over a uniform element sample -- one 32-B sector (16 words) every
 // kGuessStride words, i.e. 1/128 of the bytes, spread over the whole input
@@ -546,7 +506,7 @@ cudaError_t launch_exact_if_needed(const uint16_t* x, const StatSegs& segs, int6
   if (grid > grid_limit) grid = grid_limit;
   if (grid > ntiles) grid = ntiles;
   stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(
-      x, segs, 1, parts, done, total, book, result, need);
+      x, segs, parts, done, total, book, result, need);
   return cudaGetLastError();
 }
 
