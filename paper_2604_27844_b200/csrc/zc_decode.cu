@@ -367,7 +367,11 @@ struct __align__(128) DStage {
   uint8_t esc[kEscSlots];
 };
 constexpr int kDStageBytes = sizeof(DStage);
-constexpr int kDThreads = kThreads + 32;
+#ifndef ZC_DGROUPS
+#define ZC_DGROUPS 2
+#endif
+constexpr int kDGroups = ZC_DGROUPS;               // consumer groups of 4 warps
+constexpr int kDThreads = 32 + 128 * kDGroups;
 
 // Work is handed out dynamically in chunks of kDChunk tiles of one segment
 // (an atomic counter, claimed one chunk ahead by the producer): HBM bandwidth
@@ -386,16 +390,16 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
   DStage* ring = reinterpret_cast<DStage*>(s_dyn);
   uint64_t* full = reinterpret_cast<uint64_t*>(s_dyn + kDStages * kDStageBytes);
   uint64_t* empty = full + kDStages;
-  __shared__ __align__(16) uint32_t s_wsum[2][2][8];   // consumer group x parity x virtual warp
+  __shared__ __align__(16) uint32_t s_wsum[kDGroups][2][8];   // group x parity x virtual warp
   __shared__ HeaderInfo s_hdr[kMaxSegments];
   __shared__ int64_t s_lo[kDStages], s_al[kDStages], s_cnt[kDStages], s_tile[kDStages];
   __shared__ int32_t s_gi_shift[kDStages], s_seg[kDStages];
   __shared__ uint32_t s_spread[256];
-  __shared__ __align__(16) uint8_t s_slot[kThreads * 32];
+  __shared__ __align__(16) uint8_t s_slot[kDGroups * 128 * 32];
 
   const int tid = threadIdx.x;
   ZC_TL(0, 0);
-  if (tid >= 32) {
+  if (tid >= 32 && tid < 32 + 256) {
     const int v = tid - 32;   // byte -> nibble spread: bit k -> bit 4k
     uint32_t sp = 0;
 #pragma unroll
@@ -499,7 +503,7 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
       c = (int64_t)__shfl_sync(0xffffffffu, nx, 0);
     }
     if (lane == 0) {                  // end markers: one for each consumer group
-      for (int e = 0; e < 2; ++e, ++k) {
+      for (int e = 0; e < kDGroups; ++e, ++k) {
         const int st = (int)(k % kDStages);
         if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
         s_tile[st] = -1;
@@ -510,8 +514,8 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
   }
 
   // ========================= consumer warps ==============================
-  // Two groups of 4 warps take alternate stages (group g: k = 2i + g), so a
-  // tile is decoded by 128 threads.  Lean path (gs = 512, full tile): each
+  // kDGroups groups of 4 warps take stages in turn (group g: k = G i + g), so
+  // a tile is decoded by 128 threads.  Lean path (gs = 512, full tile): each
   // lane owns 32 consecutive words -- half the per-word fixed cost of 16 --
   // and each half-warp one 512-word group (segmented scan over 16 lanes).
   // Other tiles: two passes of the 16-word logic over virtual threads
@@ -534,7 +538,7 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
   int gsl = 0;
   bool stage_gi = false, modeA = false, gs512 = false, out_aligned = false, out_a32 = false;
   for (int64_t i = 0;; ++i) {
-    const int64_t k = 2 * i + grp;
+    const int64_t k = (int64_t)kDGroups * i + grp;
     const int st = (int)(k % kDStages);
     mbar_wait_warp(full + st, (uint32_t)((k / kDStages) & 1));
     const int64_t t = s_tile[st];
