@@ -665,7 +665,14 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
   }
   const bool esc_fast = run <= 16u * kThreads;
   uint4 ev = make_uint4(0, 0, 0, 0);
-  if (esc_fast && 16u * tid < run) ev = *reinterpret_cast<const uint4*>(esc_out + 16 * tid);
+  if (esc_fast && 16u * tid + 16u <= run) {
+    ev = *reinterpret_cast<const uint4*>(esc_out + 16 * tid);
+  } else if (esc_fast && 16u * tid < run) {   // the run's last partial 16 B: written bytes only
+    uint32_t wv[4] = {0, 0, 0, 0};
+    for (uint32_t j = 0; 16u * tid + j < run; ++j)
+      wv[j >> 2] |= (uint32_t)esc_out[16 * tid + j] << (8 * (j & 3));
+    ev = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
   // offset: the earlier runs' totals of this segment
   uint64_t acc = 0;
   for (int r = rp.run_start[seg] + tid; r < (int)blockIdx.x; r += kThreads) acc += run_total[r];

@@ -1,0 +1,83 @@
+"""Small runs of every kernel for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck): stats (certified + exact + modal), encoders (look-back,
+two-pass, speculative with a wrong guess, multi-segment), decoders (ring in
+all modes, look-back for large groups, group ranges), corrupt frames.
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_run.py
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2604_27844_b200 as zc  # noqa: E402
+from paper_2604_27844_b200 import codec, engine  # noqa: E402
+from paper_2604_27844_b200.errors import CorruptChunkError, CorruptFrameError  # noqa: E402
+
+torch.cuda.set_device(0)
+g = torch.Generator(device="cuda").manual_seed(0)
+
+
+def words(n, s=0.02):
+    return engine.words_view((torch.randn(n, device="cuda", generator=g) * s).to(torch.bfloat16))
+
+
+checks = 0
+for n, gs in [(1, 512), (1000, 16), (4096 * 20 + 7, 512), (4096 * 40, 2048), (70000, 1 << 14),
+              (5000, 4)]:
+    x = words(n)
+    book = zc.codebook_for(x)
+    chunk = zc.compress(x, book, group_size=gs)
+    assert torch.equal(zc.decompress(chunk), x)
+    ng = (n + gs - 1) // gs
+    assert torch.equal(zc.decompress_group(chunk, ng - 1), x[(ng - 1) * gs:])
+    checks += 1
+# speculative path (>= 1024 tiles): certified, and a guess the sample gets wrong
+n = 4096 * 1100 + 3
+for case in ("gauss", "fool"):
+    v = torch.randn(n, device="cuda", generator=g)
+    if case == "fool":
+        v = v * 1000.0
+        t = torch.arange(n, device="cuda")
+        v[(t % 2048) < 16] *= 1e-6          # exactly the guess kernel's sampled sectors
+    x = engine.words_view(v.to(torch.bfloat16))
+    frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    book, res, flen = engine.encode_measured(x, [(0, n)], 9, frames, [0])
+    ref = zc.serialize(zc.compress(x, zc.codebook_for(x)))
+    assert bytes(frames[:int(flen.item())].cpu().numpy()) == ref
+    checks += 1
+# multi-segment encode / decode (all-to-all framing)
+buf = words(3 * 100_003 + 5, 0.3)
+segs = [(1, 100_003), (100_004, 0), (200_007, 100_001)]
+segs = [s for s in segs if s[1]]
+caps = [engine.max_frame_bytes(c) for _, c in segs]
+offs = [0, caps[0]]
+frames = torch.empty(sum(caps), dtype=torch.uint8, device="cuda")
+_, flen = codec.device_encode(buf, segs, None, frames, offs)
+out = torch.empty(sum(c for _, c in segs), dtype=torch.int16, device="cuda")
+err = engine.decode([frames.data_ptr() + o for o in offs], [0, 0], None, [c for _, c in segs], out,
+                    [0, segs[0][1]])
+assert (err.cpu() == engine.ERR_OK).all()
+checks += 1
+# modal fallback and explicit sigma
+x = words(10_000)
+zc.codebook_for(x, sigma=0.0)
+zc.codebook_for(torch.zeros(5000, dtype=torch.int16, device="cuda"))
+checks += 1
+# corrupt frames: the validator must stay in bounds
+x = words(50_000)
+frame = bytearray(zc.serialize(zc.compress(x, zc.codebook_for(x))))
+rng = np.random.default_rng(1)
+for _ in range(20):
+    f = bytearray(frame)
+    i = int(rng.integers(128, len(f)))
+    f[i] ^= 1 << int(rng.integers(0, 8))
+    try:
+        zc.decompress(zc.parse(bytes(f)))
+    except (CorruptFrameError, CorruptChunkError):
+        pass
+checks += 1
+torch.cuda.synchronize()
+print(f"sanitize_run ok: {checks} groups of checks")
