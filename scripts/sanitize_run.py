@@ -79,5 +79,31 @@ for _ in range(20):
     except (CorruptFrameError, CorruptChunkError):
         pass
 checks += 1
+# collectives on thread ranks sharing cuda:0: NCCL-style data plane (hub) and
+# the peer-memory pull-decode (signal / wait kernels, decoder on peer frames)
+from paper_2604_27844_b200 import collectives as coll  # noqa: E402
+from paper_2604_27844_b200.transport import run_ranks  # noqa: E402
+
+
+def body(comm):
+    ok = True
+    for it in range(2):
+        local = words(200_003 + it)
+        ok &= torch.equal(coll.zip_all_gather(comm, local), coll.reference_all_gather(comm, local))
+        ok &= torch.equal(coll.zip_all_gather_p2p(comm, local),
+                          coll.reference_all_gather(comm, local))
+        sizes = [(comm.rank + d) * 3000 + 17 for d in range(comm.world_size)]
+        spec = coll.AlltoAllSpec([words(c) for c in sizes],
+                                 [(s + comm.rank) * 3000 + 17 for s in range(comm.world_size)])
+        z = coll.zip_all_to_all_p2p(comm, spec)
+        r = coll.reference_all_to_all(comm, spec)
+        ok &= all(torch.equal(a, b) for a, b in zip(z, r))
+        z = coll.zip_all_to_all_d2(comm, spec)
+        ok &= all(torch.equal(a, b) for a, b in zip(z, r))
+    return ok
+
+
+assert all(run_ranks(3, body))
+checks += 1
 torch.cuda.synchronize()
 print(f"sanitize_run ok: {checks} groups of checks")
