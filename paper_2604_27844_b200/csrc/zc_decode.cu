@@ -383,6 +383,27 @@ struct DChunkPlan {
 
 __device__ __forceinline__ uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
 
+// Dense-escape expansion (escape-heavy data): the thread's escape bytes are
+// consecutive in the staged section, eb[0 .. popc(esc)).  For every nibble of
+// esc (4 words) one unaligned 4-byte read (two aligned LDS.32 + PRMT) and one
+// PRMT with the nibble's expand selector (s_xsel: byte j <- next escape byte
+// when bit j is set, else a zero byte) OR the escape exponents into E.
+__device__ __forceinline__ void expand_escapes(const uint8_t* eb, uint32_t esc, uint32_t* E,
+                                               const uint32_t* s_xsel) {
+  uint32_t o = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t m4 = (esc >> (4 * q)) & 0xFu;
+    if (m4) {
+      const uintptr_t p = reinterpret_cast<uintptr_t>(eb + o);
+      const uint32_t* pw = reinterpret_cast<const uint32_t*>(p & ~uintptr_t(3));
+      const uint32_t src = prmt(pw[0], pw[1], 0x3210u + 0x1111u * (uint32_t)(p & 3));
+      E[q] |= prmt(src, 0u, s_xsel[m4]);
+      o += __popc(m4);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kDThreads, ZC_DMINB)   // CTAs / SM (register cap)
 decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restrict__ out,
                    int32_t* __restrict__ err, unsigned* __restrict__ counter, int write_out) {
@@ -396,6 +417,7 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
   __shared__ int32_t s_gi_shift[kDStages], s_seg[kDStages];
   __shared__ uint32_t s_spread[256];
   __shared__ __align__(16) uint8_t s_slot[kDGroups * 128 * 32];
+  __shared__ uint32_t s_xsel[16];                    // expand selectors (expand_escapes)
 
   const int tid = threadIdx.x;
   ZC_TL(0, 0);
@@ -405,6 +427,14 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
 #pragma unroll
     for (int k = 0; k < 8; ++k) sp |= ((uint32_t(v) >> k) & 1u) << (4 * k);
     s_spread[v] = sp;
+  }
+  if (tid < 16) {
+    const uint32_t m = tid;
+    uint32_t sel = 0, c = 0;
+    for (int j = 0; j < 4; ++j) {
+      sel |= (((m >> j) & 1u) ? c++ : 4u) << (4 * j);
+    }
+    s_xsel[m] = sel;
   }
   if (tid < segs.nseg) {   // every segment's header, validated once per CTA
     const HeaderInfo h = check_header(segs.stat[tid], segs.n[tid], segs.dyn_len[tid]);
@@ -602,9 +632,15 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
         E[2 * q] = prmt(tbl_lo, tbl_hi, sp);
         E[2 * q + 1] = prmt(tbl_lo, tbl_hi, sp >> 16);
       }
+      // escape-heavy warps (>= 1/4 of their words) expand all lanes' escapes
+      // with PRMT; sparse ones keep the per-escape slot loop
+      const bool dense = __shfl_sync(0xffffffffu, incl, 15) + __shfl_sync(0xffffffffu, incl, 31) >=
+                         256u;
       if (esc) {
         if (rank0 < 0 || rank0 + (int32_t)cnt > tcnt) {
           my_err = kErrZeroCount;     // accompanied by a failing index check
+        } else if (dense) {
+          expand_escapes(esc_base + rank0, esc, E, s_xsel);
         } else {
           *reinterpret_cast<uint4*>(slot) = make_uint4(0, 0, 0, 0);
           *reinterpret_cast<uint4*>(slot + 16) = make_uint4(0, 0, 0, 0);
