@@ -8,11 +8,11 @@
 
 namespace zc {
 cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
-                                     double*, int, cudaStream_t);
+                                     double*, int, cudaStream_t, bool zeroed = false);
 cudaError_t launch_codebook_modal(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
                                   cudaStream_t);
 cudaError_t launch_encode(const uint16_t*, const EncodeSegs&, const uint8_t*, uint8_t*, void*,
-                          uint64_t*, cudaStream_t);
+                          uint64_t*, cudaStream_t, bool zeroed = false);
 cudaError_t launch_decode(const DecodeSegs&, uint16_t*, int32_t*, void*, int, cudaStream_t);
 cudaError_t launch_decode_groups(const uint8_t*, int64_t, int, int64_t, int64_t, uint16_t*,
                                  cudaStream_t);

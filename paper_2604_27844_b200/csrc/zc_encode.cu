@@ -802,15 +802,26 @@ static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, co
   return cudaGetLastError();
 }
 
+cudaError_t launch_encode(const uint16_t*, const EncodeSegs&, const uint8_t*, uint8_t*, void*,
+                          uint64_t*, cudaStream_t, bool zeroed = false);
+
+// Look-back encoder state: counter at ws[0], tile status words behind the
+// statistic's counters and partials (ws[64, 128 + 32 x grid) stays theirs),
+// so one memset of [0, kLbStatusOff + 8 x tiles) serves a measured encode.
+constexpr int64_t kLbStatusOff = 256 + 8 * 4096;
+
 cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8_t* book,
-                          uint8_t* frames, void* ws, uint64_t* frame_len, cudaStream_t st) {
+                          uint8_t* frames, void* ws, uint64_t* frame_len, cudaStream_t st,
+                          bool zeroed) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
   uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
   if (ntiles <= kLookbackMaxTiles) {
     unsigned* counter = reinterpret_cast<unsigned*>(w8);
-    uint64_t* status = reinterpret_cast<uint64_t*>(w8 + 128);
-    cudaError_t e = cudaMemsetAsync(ws, 0, 128 + 8 * ntiles, st);
-    if (e != cudaSuccess) return e;
+    uint64_t* status = reinterpret_cast<uint64_t*>(w8 + kLbStatusOff);
+    if (!zeroed) {
+      cudaError_t e = cudaMemsetAsync(ws, 0, kLbStatusOff + 8 * ntiles, st);
+      if (e != cudaSuccess) return e;
+    }
     static int cap = 0;
     if (cap == 0) cap = grid_for((const void*)encode_lookback_kernel, kThreads, 0);
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
@@ -824,7 +835,7 @@ cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8
 }
 
 cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
-                                     double*, int, cudaStream_t);
+                                     double*, int, cudaStream_t, bool zeroed = false);
 cudaError_t launch_guess(const uint16_t*, const StatSegs&, void*, unsigned*, uint8_t*,
                          cudaStream_t);
 cudaError_t launch_exact_if_needed(const uint16_t*, const StatSegs&, int64_t, Partial*, unsigned*,
@@ -850,9 +861,16 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   const int64_t ntiles = segs.tile_start[segs.nseg];
   uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
   if (!speculative || ntiles < kSpecMinTiles) {
-    cudaError_t e = launch_codebook_measured(x, ss, total, ws, book, result, 0, st);
+    // small inputs: one memset for the statistic's and the look-back
+    // encoder's counters (fewer graph nodes on the latency-bound path)
+    const bool merged = ntiles <= kLookbackMaxTiles;
+    if (merged) {
+      cudaError_t e = cudaMemsetAsync(ws, 0, kLbStatusOff + 8 * ntiles, st);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = launch_codebook_measured(x, ss, total, ws, book, result, 0, st, merged);
     if (e != cudaSuccess) return e;
-    return launch_encode(x, segs, book, frames, ws, frame_len, st);
+    return launch_encode(x, segs, book, frames, ws, frame_len, st, merged);
   }
   const RunPlan rp = make_plan(segs, tiles_cap());
   if (rp.nruns > 4096) return cudaErrorInvalidValue;

@@ -354,10 +354,15 @@ __global__ void mode_kernel(const unsigned long long* __restrict__ hist, int64_t
 // exact != 0: result[0] must be the f64 statistic itself (measure_sigma);
 // otherwise the certified pass decides the codebook and the exact kernel
 // returns at once unless the certificate failed.
+// Small inputs skip the certified pass: the exact kernel alone is one launch
+// fewer, and its f64 work is negligible at this size.
+constexpr int64_t kSmallExactTiles = 16;
+
 cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, int64_t total,
                                      void* ws, uint8_t* book, double* result, int exact,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, bool zeroed) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
+  if (ntiles <= kSmallExactTiles) exact = 1;
   uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
   Partial* parts = reinterpret_cast<Partial*>(w8 + 128);
   const int cap = stats_grid_cap();
@@ -366,8 +371,10 @@ cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, in
   unsigned* done_sums = reinterpret_cast<unsigned*>(w8 + 68);
   int* need = reinterpret_cast<int*>(w8 + 72);
   if (grid > 0) {
-    cudaError_t e = cudaMemsetAsync(done, 0, 16, st);
-    if (e != cudaSuccess) return e;
+    if (!zeroed) {   // else the caller cleared [64, 80) of ws in its own memset
+      cudaError_t e = cudaMemsetAsync(done, 0, 16, st);
+      if (e != cudaSuccess) return e;
+    }
     if (!exact) {
       const int scap = sums_grid_cap();
       const int64_t sgrid = ntiles < scap ? ntiles : scap;
