@@ -385,18 +385,21 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
   uint32_t run = 0;   // escapes of this run before the current tile
   double s1 = 0.0, s2 = 0.0;   // fused certified statistic (kSums), unshifted (K = 0)
   // ---- lean loop: aligned input, tile fully inside the segment ---------------
+  // Tiles are taken two at a time: both tiles' words are encoded, one CTA scan
+  // covers both (the second tile's escapes follow the first's), so the two
+  // block barriers are paid once per 8192 words instead of once per 4096
+  // (measured ~1 %: the kernel is close to issue-bound, not barrier-bound).
   const int64_t t_full_end = aligned ? ((n / kTile) < t_end ? (n / kTile) : t_end) : t_begin;
-  const int nfast = (int)(t_full_end > t_begin ? t_full_end - t_begin : 0);
+  int nfast = (int)(t_full_end > t_begin ? t_full_end - t_begin : 0);
+  nfast &= ~1;                        // an odd last full tile goes to the general loop
   {
-    uint8_t* p_sm = frame + L.off[0] + t_begin * kTile + tid * kEPT;
-    uint8_t* p_pl0 = frame + L.off[1] + (t_begin * kTile + tid * kEPT) / 8;
     const int64_t pl_stride = L.off[2] - L.off[1];
-    uint32_t* gi_w = gi + ((t_begin * kTile + tid * kEPT) >> 9);
     const bool gi512 = gsl == 9;
-    for (int k = 0; k < nfast; ++k) {
-      const int st = (int)((unsigned)k % (unsigned)kStages);
+    __shared__ __align__(16) uint32_t s_warp2[2][kWarps];
+    // encode this thread's 16 words of local tile k (stage st): sign-mantissa
+    // and plane bytes stored; returns the escape mask
+    auto encode16 = [&](int k, int st) -> uint32_t {
       const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
-      mbar_wait_warp(bars + st, (uint32_t)((k / kStages) & 1));
       const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
       const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
       const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
@@ -423,32 +426,28 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
                                      : __umulhi(wl & 0x00007F80u, 1u << 27);
         B += *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(s_lut) + off) << j;
       }
-      st_stream_v4(p_sm, make_uint4(sm[0], sm[1], sm[2], sm[3]));
+      const int64_t e0 = (t_begin + k) * kTile + tid * kEPT;
+      st_stream_v4(frame + L.off[0] + e0, make_uint4(sm[0], sm[1], sm[2], sm[3]));
+      uint8_t* p_pl0 = frame + L.off[1] + (e0 >> 3);
       *reinterpret_cast<uint16_t*>(p_pl0) = (uint16_t)prmt(A, B, 0x40);
       *reinterpret_cast<uint16_t*>(p_pl0 + pl_stride) = (uint16_t)prmt(A, B, 0x51);
       *reinterpret_cast<uint16_t*>(p_pl0 + 2 * pl_stride) = (uint16_t)prmt(A, B, 0x62);
-      const uint32_t esc = prmt(A, B, 0x73) & 0xFFFFu;
-      const uint32_t cnt = __popc(esc);
-      uint32_t incl = warp_incl_scan(cnt);
-      if (lane == 31) s_warp[warp] = incl;
-      __syncthreads();                                    // (B)
-      const uint32_t wv = lane < kWarps ? s_warp[lane] : 0u;
-      uint32_t wi = warp_incl_scan<kWarps>(wv);
-      const uint32_t wbase = __shfl_sync(0xffffffffu, wi - wv, warp);
-      const uint32_t agg = __shfl_sync(0xffffffffu, wi, kWarps - 1);
-      const uint32_t lp = run + wbase + incl - cnt;
+      return prmt(A, B, 0x73) & 0xFFFFu;
+    };
+    // group_index entries and escape bytes of local tile k, run prefix lp
+    auto place16 = [&](int k, int st, uint32_t esc, uint32_t lp) {
+      const int64_t base = (t_begin + k) * kTile + (int64_t)tid * kEPT;
       if (gi512) {
-        if (lane == 0) *gi_w = lp;
+        if (lane == 0) gi[base >> 9] = lp;
       } else if (gsl >= 4) {
-        const int64_t base = (t_begin + k) * kTile + (int64_t)tid * kEPT;
         if ((base & ((int64_t(1) << gsl) - 1)) == 0) gi[base >> gsl] = lp;
       } else {
-        const int64_t base = (t_begin + k) * kTile + (int64_t)tid * kEPT;
         const int gs = 1 << gsl;
         for (int j = 0; j < kEPT; j += gs)
           gi[(base + j) >> gsl] = lp + __popc(esc & ((1u << j) - 1u));
       }
       if (esc) {
+        const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
         uint8_t* dst = esc_out + lp;
         uint32_t m = esc;
         while (m) {
@@ -457,15 +456,41 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
           *dst++ = (uint8_t)((tw[tid * kEPT + j] >> 7) & 0xFFu);
         }
       }
-      run += agg;
-      __syncthreads();                                    // (C) stage + s_warp free
-      if (tid == 0 && t_begin + k + kStages < t_end) {
-        fence_proxy_async();
-        encode_issue(xs, n, t_begin + k + kStages, ring + st * kStageBytes, bars + st);
+    };
+    for (int k = 0; k < nfast; k += 2) {
+      const int st0 = (int)((unsigned)k % (unsigned)kStages);
+      const int st1 = (int)((unsigned)(k + 1) % (unsigned)kStages);
+      mbar_wait_warp(bars + st0, (uint32_t)((k / kStages) & 1));
+      const uint32_t esc0 = encode16(k, st0);
+      mbar_wait_warp(bars + st1, (uint32_t)(((k + 1) / kStages) & 1));
+      const uint32_t esc1 = encode16(k + 1, st1);
+      const uint32_t cnt0 = __popc(esc0), cnt1 = __popc(esc1);
+      const uint32_t incl0 = warp_incl_scan(cnt0);
+      const uint32_t incl1 = warp_incl_scan(cnt1);
+      if (lane == 31) {
+        s_warp2[0][warp] = incl0;
+        s_warp2[1][warp] = incl1;
       }
-      p_sm += kTile;
-      p_pl0 += kTile / 8;
-      gi_w += kTile / 512;
+      __syncthreads();                                    // (B)
+      const uint32_t v0 = lane < kWarps ? s_warp2[0][lane] : 0u;
+      const uint32_t v1 = lane < kWarps ? s_warp2[1][lane] : 0u;
+      const uint32_t wi0 = warp_incl_scan<kWarps>(v0);
+      const uint32_t wi1 = warp_incl_scan<kWarps>(v1);
+      const uint32_t wbase0 = __shfl_sync(0xffffffffu, wi0 - v0, warp);
+      const uint32_t wbase1 = __shfl_sync(0xffffffffu, wi1 - v1, warp);
+      const uint32_t agg0 = __shfl_sync(0xffffffffu, wi0, kWarps - 1);
+      const uint32_t agg1 = __shfl_sync(0xffffffffu, wi1, kWarps - 1);
+      place16(k, st0, esc0, run + wbase0 + incl0 - cnt0);
+      place16(k + 1, st1, esc1, run + agg0 + wbase1 + incl1 - cnt1);
+      run += agg0 + agg1;
+      __syncthreads();                                    // (C) stages + s_warp2 free
+      if (tid == 0) {
+        fence_proxy_async();
+        if (t_begin + k + kStages < t_end)
+          encode_issue(xs, n, t_begin + k + kStages, ring + st0 * kStageBytes, bars + st0);
+        if (t_begin + k + 1 + kStages < t_end)
+          encode_issue(xs, n, t_begin + k + 1 + kStages, ring + st1 * kStageBytes, bars + st1);
+      }
     }
   }
   for (int64_t t = t_begin + nfast; t < t_end; ++t) {
