@@ -8,6 +8,7 @@ All tensors are CUDA tensors; BF16 words travel as int16 (same bits).
 from __future__ import annotations
 
 import functools
+import threading
 
 import torch
 
@@ -28,21 +29,49 @@ def words_view(t: torch.Tensor) -> torch.Tensor:
 
 
 _WS: dict = {}
+_WS_LOCKS: dict = {}
+_WS_GUARD = threading.Lock()
 
 
-def workspace(total_elems: int, nseg: int, device, stream=None) -> torch.Tensor:
+class _Workspace:
+    """A workspace buffer and the lock that keeps one call's launches
+    contiguous on its stream (ctypes releases the GIL, so two host threads
+    driving the same stream could otherwise interleave their kernels over the
+    shared scratch)."""
+
+    def __init__(self, buf, lock):
+        self.buf, self.lock = buf, lock
+
+    def data_ptr(self):
+        return self.buf.data_ptr()
+
+    def numel(self):
+        return self.buf.numel()
+
+    def __enter__(self):
+        self.lock.acquire()
+        return self
+
+    def __exit__(self, *exc):
+        self.lock.release()
+
+
+def workspace(total_elems: int, nseg: int, device, stream=None) -> _Workspace:
     """Scratch for one call.  Cached per (device, stream) and grown on demand,
     so steady-state calls (and CUDA-graph captures) allocate nothing; calls on
-    one stream are ordered, so reuse is safe."""
+    one stream are ordered, so reuse is safe as long as each call's launches
+    are enqueued under the workspace lock (``with workspace(...) as ws:``)."""
     nbytes = int(lib().zc_workspace_bytes(int(total_elems), int(nseg)))
     dev = torch.device(device)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     key = (dev.index, int(s.cuda_stream))
-    buf = _WS.get(key)
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
-        _WS[key] = buf
-    return buf
+    with _WS_GUARD:
+        lock = _WS_LOCKS.setdefault(key, threading.RLock())
+        buf = _WS.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            _WS[key] = buf
+    return _Workspace(buf, lock)
 
 
 @functools.lru_cache(maxsize=1024)
@@ -74,13 +103,12 @@ def measured_codebook(words: torch.Tensor, segs=None, stream=None, exact: bool =
     book = torch.empty(8, dtype=torch.uint8, device=dev)
     result = torch.empty(3, dtype=torch.float64, device=dev)
     total = sum(n for _, n in segs)
-    ws = workspace(total, len(segs), dev, stream)
-    st = check(lib().zc_codebook_measured(
-        words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
-        i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
-        result.data_ptr(), SIGMA_EXACT if exact else 0, stream_ptr(stream)),
-        "zc_codebook_measured")
-    del st
+    with workspace(total, len(segs), dev, stream) as ws:
+        check(lib().zc_codebook_measured(
+            words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
+            i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
+            result.data_ptr(), SIGMA_EXACT if exact else 0, stream_ptr(stream)),
+            "zc_codebook_measured")
     return book, result
 
 
@@ -91,11 +119,11 @@ def modal_codebook(words: torch.Tensor, segs=None, stream=None) -> torch.Tensor:
     dev = words.device
     book = torch.empty(8, dtype=torch.uint8, device=dev)
     total = sum(n for _, n in segs)
-    ws = workspace(total, len(segs), dev, stream)
-    check(lib().zc_codebook_modal(
-        words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
-        i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
-        stream_ptr(stream)), "zc_codebook_modal")
+    with workspace(total, len(segs), dev, stream) as ws:
+        check(lib().zc_codebook_modal(
+            words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
+            i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
+            stream_ptr(stream)), "zc_codebook_modal")
     return book
 
 
@@ -119,14 +147,15 @@ def encode(words: torch.Tensor, segs, book: torch.Tensor, gs_log2: int,
     if frame_len is None:
         frame_len = torch.empty(nseg, dtype=torch.int64, device=words.device)
     total = sum(n for _, n in segs)
-    ws = workspace(total, nseg, words.device, stream)
-    for lo in range(0, nseg, _lib.MAX_SEGMENTS):
-        part = segs[lo:lo + _lib.MAX_SEGMENTS]
-        offs = list(frame_offs)[lo:lo + _lib.MAX_SEGMENTS]
-        check(lib().zc_encode(
-            words.data_ptr(), i64s(o for o, _ in part), i64s(n for _, n in part), i64s(offs),
-            len(part), book.data_ptr(), int(gs_log2), frames.data_ptr(), ws.data_ptr(),
-            ws.numel(), frame_len.data_ptr() + 8 * lo, stream_ptr(stream)), "zc_encode")
+    with workspace(total, nseg, words.device, stream) as ws:
+        for lo in range(0, nseg, _lib.MAX_SEGMENTS):
+            part = segs[lo:lo + _lib.MAX_SEGMENTS]
+            offs = list(frame_offs)[lo:lo + _lib.MAX_SEGMENTS]
+            check(lib().zc_encode(
+                words.data_ptr(), i64s(o for o, _ in part), i64s(n for _, n in part),
+                i64s(offs), len(part), book.data_ptr(), int(gs_log2), frames.data_ptr(),
+                ws.data_ptr(), ws.numel(), frame_len.data_ptr() + 8 * lo, stream_ptr(stream)),
+                "zc_encode")
     return frame_len
 
 
@@ -147,12 +176,12 @@ def encode_measured(words: torch.Tensor, segs, gs_log2: int, frames: torch.Tenso
     book = torch.empty(8, dtype=torch.uint8, device=dev)
     result = torch.empty(3, dtype=torch.float64, device=dev)
     total = sum(n for _, n in segs)
-    ws = workspace(total, nseg, dev, stream)
-    check(lib().zc_encode_measured(
-        words.data_ptr(), i64s(o for o, _ in segs), i64s(n for _, n in segs), i64s(frame_offs),
-        nseg, int(gs_log2), frames.data_ptr(), ws.data_ptr(), ws.numel(), frame_len.data_ptr(),
-        book.data_ptr(), result.data_ptr(), 1 if speculative else 0, stream_ptr(stream)),
-        "zc_encode_measured")
+    with workspace(total, nseg, dev, stream) as ws:
+        check(lib().zc_encode_measured(
+            words.data_ptr(), i64s(o for o, _ in segs), i64s(n for _, n in segs),
+            i64s(frame_offs), nseg, int(gs_log2), frames.data_ptr(), ws.data_ptr(), ws.numel(),
+            frame_len.data_ptr(), book.data_ptr(), result.data_ptr(),
+            1 if speculative else 0, stream_ptr(stream)), "zc_encode_measured")
     return book, result, frame_len
 
 
@@ -172,16 +201,16 @@ def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_
     if err is None:
         err = torch.empty(nseg, dtype=torch.int32, device=dev)
     total = sum(int(c) for c in counts)
-    ws = workspace(total, nseg, dev, stream)
-    for lo in range(0, nseg, _lib.MAX_SEGMENTS):
-        hi = lo + _lib.MAX_SEGMENTS
-        check(lib().zc_decode(
-            ptrs(stat_ptrs[lo:hi]), ptrs(dyn_ptrs[lo:hi]),
-            i64s(dyn_lens[lo:hi]) if dyn_lens is not None else None,
-            i64s(counts[lo:hi]), i64s(out_offs[lo:hi]) if out_offs is not None else None,
-            len(counts[lo:hi]), out.data_ptr() if out is not None else None,
-            err.data_ptr() + 4 * lo, ws.data_ptr(), ws.numel(), flags,
-            stream_ptr(stream)), "zc_decode")
+    with workspace(total, nseg, dev, stream) as ws:
+        for lo in range(0, nseg, _lib.MAX_SEGMENTS):
+            hi = lo + _lib.MAX_SEGMENTS
+            check(lib().zc_decode(
+                ptrs(stat_ptrs[lo:hi]), ptrs(dyn_ptrs[lo:hi]),
+                i64s(dyn_lens[lo:hi]) if dyn_lens is not None else None,
+                i64s(counts[lo:hi]), i64s(out_offs[lo:hi]) if out_offs is not None else None,
+                len(counts[lo:hi]), out.data_ptr() if out is not None else None,
+                err.data_ptr() + 4 * lo, ws.data_ptr(), ws.numel(), flags,
+                stream_ptr(stream)), "zc_decode")
     return err
 
 

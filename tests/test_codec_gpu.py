@@ -338,3 +338,33 @@ def test_profile_hooks_record_encoder_and_decoder_launches():
     assert len(enc) == 3 and len(dec) == 3
     assert all(t > 0 for t in enc + dec)
     assert torch.equal(out, x)
+
+
+def test_two_host_threads_share_a_stream():
+    # ctypes releases the GIL inside the C calls: two threads driving the same
+    # stream must not interleave their launches over the shared workspace
+    import threading
+    stream = torch.cuda.current_stream()
+    results = {}
+
+    def work(tid):
+        torch.cuda.set_device(0)
+        ok = True
+        with torch.cuda.stream(stream):
+            for it in range(6):
+                n = 4096 * (300 + 37 * tid) + it
+                x = engine.words_view((torch.randn(n, device="cuda") * (0.02 + tid)).to(
+                    torch.bfloat16))
+                frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+                _, _, flen = engine.encode_measured(x, [(0, n)], 9, frames, [0])
+                out = torch.empty_like(x)
+                err = engine.decode([frames.data_ptr()], [0], None, [n], out, [0])
+                ok &= int(err.item()) == engine.ERR_OK and torch.equal(out, x)
+        results[tid] = ok
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert results == {0: True, 1: True}
