@@ -70,7 +70,18 @@ def _seam_worker(rank, world, port, q):
     got = comm.exchange_sizes(sizes)
     gathered = comm.allgather_ints(7 + rank)
     comm.barrier()
-    q.put((rank, got, gathered, comm.stats.bytes_sent))
+    sent = comm.stats.bytes_sent
+    # the byte movers of the N>1 data planes (static / dynamic sections)
+    import torch
+    from paper_2604_27844_b200.collectives import allgather_scalar
+    mine = torch.arange(5, dtype=torch.uint8) + 10 * rank
+    allg = torch.empty(5 * world, dtype=torch.uint8)
+    comm.all_gather_bytes(mine, allg)
+    peer = 1 - rank
+    recv = {peer: torch.empty(3 + peer, dtype=torch.uint8)}
+    comm.sendrecv_bytes({peer: torch.full((3 + rank,), 50 + rank, dtype=torch.uint8)}, recv)
+    scal = allgather_scalar(comm, 0.5 + rank)
+    q.put((rank, got, gathered, sent, allg.tolist(), recv[peer].tolist(), scal))
     dist.destroy_process_group()
 
 
@@ -82,12 +93,16 @@ def test_exchange_sizes_transpose_over_gloo():
     procs = [ctx.Process(target=_seam_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict((r, (g, a, b)) for r, g, a, b in (q.get(timeout=120) for _ in procs))
+    res = dict((v[0], v[1:]) for v in (q.get(timeout=120) for _ in procs))
     for p in procs:
         p.join(timeout=60)
     for r in range(world):
-        got, gathered, sent = res[r]
+        got, gathered, sent, allg, recv, scal = res[r]
         # entry p = what peer p declared for this rank; self passes through
         assert got == [100 * p + r if p != r else 100 * r + r for p in range(world)]
         assert gathered == [7, 8]
         assert sent == 8 * (world - 1)
+        assert allg == [i + 10 * q for q in range(world) for i in range(5)]
+        peer = 1 - r
+        assert recv == [50 + peer] * (3 + peer)
+        assert scal == [0.5, 1.5]
