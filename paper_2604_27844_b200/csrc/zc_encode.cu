@@ -434,8 +434,8 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       *reinterpret_cast<uint16_t*>(p_pl0 + 2 * pl_stride) = (uint16_t)prmt(A, B, 0x62);
       return prmt(A, B, 0x73) & 0xFFFFu;
     };
-    // group_index entries and escape bytes of local tile k, run prefix lp
-    auto place16 = [&](int k, int st, uint32_t esc, uint32_t lp) {
+    // group_index entries of local tile k, run prefix lp
+    auto place_gi = [&](int k, uint32_t esc, uint32_t lp) {
       const int64_t base = (t_begin + k) * kTile + (int64_t)tid * kEPT;
       if (gi512) {
         if (lane == 0) gi[base >> 9] = lp;
@@ -445,16 +445,6 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
         const int gs = 1 << gsl;
         for (int j = 0; j < kEPT; j += gs)
           gi[(base + j) >> gsl] = lp + __popc(esc & ((1u << j) - 1u));
-      }
-      if (esc) {
-        const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
-        uint8_t* dst = esc_out + lp;
-        uint32_t m = esc;
-        while (m) {
-          const int j = __ffs(m) - 1;
-          m &= m - 1;
-          *dst++ = (uint8_t)((tw[tid * kEPT + j] >> 7) & 0xFFu);
-        }
       }
     };
     for (int k = 0; k < nfast; k += 2) {
@@ -480,8 +470,28 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       const uint32_t wbase1 = __shfl_sync(0xffffffffu, wi1 - v1, warp);
       const uint32_t agg0 = __shfl_sync(0xffffffffu, wi0, kWarps - 1);
       const uint32_t agg1 = __shfl_sync(0xffffffffu, wi1, kWarps - 1);
-      place16(k, st0, esc0, run + wbase0 + incl0 - cnt0);
-      place16(k + 1, st1, esc1, run + agg0 + wbase1 + incl1 - cnt1);
+      const uint32_t lp0 = run + wbase0 + incl0 - cnt0;
+      const uint32_t lp1 = run + agg0 + wbase1 + incl1 - cnt1;
+      place_gi(k, esc0, lp0);
+      place_gi(k + 1, esc1, lp1);
+      // escape bytes of both tiles in one loop (codec.py:283-284): bits of
+      // m = esc0 | esc1 << 16 highest first, so a warp loops max(cnt0 + cnt1)
+      // times; a bit's slot is its tile's prefix + the bits left below it
+      uint32_t m = esc0 | (esc1 << 16);
+      if (m) {
+        const uint32_t a0 = smem_u32(ring + st0 * kStageBytes) + tid * (2 * kEPT);
+        const uint32_t a1 = smem_u32(ring + st1 * kStageBytes) + tid * (2 * kEPT) - 32u;
+        const uint32_t o1 = lp1 - cnt0;
+        do {
+          uint32_t j, b, v;
+          asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(m));
+          asm("shl.b32 %0, 1, %1;" : "=r"(b) : "r"(j));
+          m ^= b;
+          const bool hi = j >= 16u;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"((hi ? a1 : a0) + 2u * j));
+          esc_out[(hi ? o1 : lp0) + __popc(m)] = (uint8_t)(v >> 7);
+        } while (m);
+      }
       run += agg0 + agg1;
       __syncthreads();                                    // (C) stages + s_warp2 free
       if (tid == 0) {
