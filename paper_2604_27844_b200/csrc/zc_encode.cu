@@ -398,12 +398,12 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     __shared__ __align__(16) uint32_t s_warp2[2][kWarps];
     // encode this thread's 16 words of local tile k (stage st): sign-mantissa
     // and plane bytes stored; returns the escape mask
-    auto encode16 = [&](int k, int st) -> uint32_t {
+    auto encode16 = [&](int k, int st, uint64_t& c1, uint64_t& c2) -> uint32_t {
       const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
       const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
       const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
       const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      if (kSums) sums_acc16_k0(w, s1, s2);
+      if (kSums) sums_chain16_k0(w, c1, c2);
       uint32_t sm[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -448,12 +448,17 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       }
     };
     for (int k = 0; k < nfast; k += 2) {
+      uint64_t c1 = 0, c2 = 0;   // packed fp32 chains of the pair (kSums)
       const int st0 = (int)((unsigned)k % (unsigned)kStages);
       const int st1 = (int)((unsigned)(k + 1) % (unsigned)kStages);
       mbar_wait_warp(bars + st0, (uint32_t)((k / kStages) & 1));
-      const uint32_t esc0 = encode16(k, st0);
+      const uint32_t esc0 = encode16(k, st0, c1, c2);
       mbar_wait_warp(bars + st1, (uint32_t)(((k + 1) / kStages) & 1));
-      const uint32_t esc1 = encode16(k + 1, st1);
+      const uint32_t esc1 = encode16(k + 1, st1, c1, c2);
+      if (kSums) {
+        s1 += f2_sum(c1);
+        s2 += f2_sum(c2);
+      }
       const uint32_t cnt0 = __popc(esc0), cnt1 = __popc(esc1);
       const uint32_t incl0 = warp_incl_scan(cnt0);
       const uint32_t incl1 = warp_incl_scan(cnt1);

@@ -169,6 +169,17 @@ __device__ __forceinline__ void sums_acc16_k0(const uint32_t* w, double& s1, dou
   s2 += f2_sum(a2);
 }
 
+// Packed accumulation only (the caller flushes with f2_sum): the fused
+// encoder chains two tiles' words, 16 terms per fp32 lane.
+__device__ __forceinline__ void sums_chain16_k0(const uint32_t* w, uint64_t& a1, uint64_t& a2) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint64_t v = (uint64_t)(w[j] & 0xFFFF0000u) << 32 | (uint64_t)(w[j] << 16);
+    a1 = f2_add(a1, v);
+    a2 = f2_fma(v, v, a2);
+  }
+}
+
 // Shift word pair of the certified statistic: K = the first element of the
 // concatenation when finite, else 0, in both halves (d = x - K per element).
 __device__ __forceinline__ uint64_t sums_shift(uint32_t kw) {
@@ -236,13 +247,13 @@ __device__ inline void write_window(uint8_t* book, int base) {
 // ---- certified fast statistic ------------------------------------------------
 // Every element contributes d = x - K (K = the first element when finite, else
 // 0; the same K everywhere, so partials merge by plain addition) to per-tile
-// sums kept in packed fp32 (FADD2/FFMA2, 8 terms per lane), flushed to f64
-// once per tile.  A non-finite element poisons the sums (inf/NaN propagate),
+// sums kept in packed fp32 (FADD2/FFMA2, at most 16 terms per lane), flushed
+// to f64 once per tile (the fused encoder: once per tile pair).  A non-finite element poisons the sums (inf/NaN propagate),
 // which routes the call to the exact f64 kernel.  Error bound (u = 2^-24):
-// per element fl(x - K) = d(1+δ), |δ| <= u; 8-term fp32 chains add <= γ_8;
+// per element fl(x - K) = d(1+δ), |δ| <= u; 16-term fp32 chains add <= γ_16;
 // f64 accumulation adds <= 2^-36 relative; with Q = Σd² (>= 0) and
-// |S1| <= sqrt(N Q):  |ΔS2| <= 11u·Q, |ΔS1| <= 10u·Σ|d|, so
-//   |ΔM2| = |ΔS2 - (2 S1 ΔS1 + ΔS1²)/N| <= 32u·Q + 2^-34·Q + N·2^-149
+// |S1| <= sqrt(N Q):  |ΔS2| <= 19u·Q, |ΔS1| <= 18u·Σ|d|, so
+//   |ΔM2| = |ΔS2 - (2 S1 ΔS1 + ΔS1²)/N| <= 64u·Q + 2^-34·Q + N·2^-149
 // (the last term: fp32 underflow of d², also in the bound on Q).  The codebook is certified when
 // derive_base() agrees at both ends of sigma = sqrt((M2 ± Δ)/N), widened by
 // 2^-40 for the reference's own f64 evaluation (np.std two-pass error); the
@@ -274,7 +285,7 @@ __device__ inline void certify_block(const SumPartial* parts, int64_t nparts, in
   if (total > 0 && isfinite(S1) && isfinite(S2)) {
     const double m2 = S2 - S1 * (S1 / N);
     const double q = S2 * (1.0 + 0x1p-20);                 // >= true Q
-    const double delta = (32.0 * 0x1p-24 + 0x1p-34) * q + N * 0x1p-149;
+    const double delta = (64.0 * 0x1p-24 + 0x1p-34) * q + N * 0x1p-149;
     if (m2 - delta > 0.0) {
       const double s_lo = sqrt((m2 - delta) / N) * (1.0 - 0x1p-40);
       const double s_hi = sqrt((m2 + delta) / N) * (1.0 + 0x1p-40);
