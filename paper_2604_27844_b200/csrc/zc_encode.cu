@@ -483,7 +483,51 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       // m = esc0 | esc1 << 16 highest first, so a warp loops max(cnt0 + cnt1)
       // times; a bit's slot is its tile's prefix + the bits left below it
       uint32_t m = esc0 | (esc1 << 16);
-      if (m) {
+      if (__builtin_expect(agg0 + agg1 >= 2048u, 0)) {
+        // escape-heavy pair (>= 1/4 of the CTA's words): each lane's escape
+        // bytes go to its warp's shared slot at the warp-local prefix, then
+        // the warp copies its contiguous run out with coalesced byte stores
+        // (per-lane byte stores scatter each warp-wide store over ~13
+        // sectors: 2x slower on the C4 outlier mixes)
+        // The slot is the first half of the warp's own 1 KB of the input
+        // stage: read into registers first, the stage is refilled only after
+        // barrier (C).  Block barriers (the branch is CTA-uniform) and warp
+        // totals from s_warp2: a __syncwarp / shuffle here cost the model-data
+        // loop 2 us although never executed.
+        auto dense16s = [&](int st, uint32_t esc, uint32_t excl, uint32_t wtot, uint32_t lp) {
+          uint8_t* sb = ring + st * kStageBytes + warp * (2 * kEPT * 32);
+          const uint16_t* tw = reinterpret_cast<const uint16_t*>(ring + st * kStageBytes);
+          const uint4 a = *reinterpret_cast<const uint4*>(tw + tid * kEPT);
+          const uint4 b = *reinterpret_cast<const uint4*>(tw + tid * kEPT + 8);
+          // exponent bytes of 4 words per register
+          const uint32_t e4[4] = {
+              (prmt(a.x, a.y, 0x7531) << 1 & 0xFEFEFEFEu) | (prmt(a.x, a.y, 0x6420) >> 7 & 0x01010101u),
+              (prmt(a.z, a.w, 0x7531) << 1 & 0xFEFEFEFEu) | (prmt(a.z, a.w, 0x6420) >> 7 & 0x01010101u),
+              (prmt(b.x, b.y, 0x7531) << 1 & 0xFEFEFEFEu) | (prmt(b.x, b.y, 0x6420) >> 7 & 0x01010101u),
+              (prmt(b.z, b.w, 0x7531) << 1 & 0xFEFEFEFEu) | (prmt(b.z, b.w, 0x6420) >> 7 & 0x01010101u)};
+          __syncthreads();
+          // shared accesses as asm without a memory clobber: ordered by the
+          // block barriers around them, invisible to the compiler's alias
+          // analysis of the hot loop (plain C++ stores here cost it 2 us)
+          uint32_t p = smem_u32(sb) + excl;
+#pragma unroll
+          for (int j = 0; j < kEPT; ++j)
+            if (esc & (1u << j)) {
+              asm volatile("st.shared.u8 [%0], %1;" ::"r"(p), "r"(e4[j >> 2] >> (8 * (j & 3))));
+              ++p;
+            }
+          __syncthreads();
+          uint8_t* dst = esc_out + (lp - excl);          // the warp's first escape
+          const uint32_t sb32 = smem_u32(sb);
+          for (uint32_t i = lane; i < wtot; i += 32) {
+            uint32_t v;
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sb32 + i));
+            dst[i] = (uint8_t)v;
+          }
+        };
+        dense16s(st0, esc0, incl0 - cnt0, s_warp2[0][warp], lp0);
+        dense16s(st1, esc1, incl1 - cnt1, s_warp2[1][warp], lp1);
+      } else if (m) {
         const uint32_t a0 = smem_u32(ring + st0 * kStageBytes) + tid * (2 * kEPT);
         const uint32_t a1 = smem_u32(ring + st1 * kStageBytes) + tid * (2 * kEPT) - 32u;
         const uint32_t o1 = lp1 - cnt0;

@@ -153,6 +153,27 @@ def test_fuzz_buffers_against_oracle():
         assert np.array_equal(host_words(zc.decompress(zc.parse(frame))), w)
 
 
+@pytest.mark.parametrize("gs", [4, 16, 512, 2048])
+def test_escape_density_mix_two_pass_against_oracle(gs):
+    # >= 32 tiles (two-pass encoder, tile-pair lean loop) whose 1024-word
+    # blocks cycle through escape densities 0 .. 100 %: warps on both sides
+    # of the encoder's dense-escape switch (1/4 of a warp's words), runs that
+    # mix them, an odd tail tile and a partial last tile
+    rng = np.random.default_rng(gs)
+    n = 4096 * 81 + 1234
+    w = np.asarray(zo.gaussian(n, 1.0, seed=gs), dtype=np.uint16).copy()
+    book = codec.derive_codebook(1.0)
+    fr = [0.0, 0.02, 0.1, 0.2, 0.24, 0.26, 0.3, 0.5, 0.75, 0.9, 1.0]
+    for b in range(0, n, 1024):
+        f = fr[(b // 1024) % len(fr)]
+        m = rng.random(min(1024, n - b)) < f
+        # exponent 1 (tiny normals): outside any sigma = 1 window
+        w[b:b + m.size][m] = (w[b:b + m.size][m] & 0x807F) | (1 << 7)
+    frame = zc.serialize(zc.compress(w, book, gs))
+    assert frame == zo.encode(w, book.entries, gs)
+    assert np.array_equal(host_words(zc.decompress(zc.parse(frame))), w)
+
+
 @pytest.mark.parametrize("n", [1 << 27, 218112000 // 8, 5 * 4096 * 4096 + 3])
 def test_large_round_trip_properties(n):
     # size-independent properties at benchmark scale: decode(encode(x)) == x,
