@@ -379,6 +379,7 @@ constexpr int kDThreads = 32 + 128 * kDGroups;
 // between 79 and 150 us of a 150 us launch (scripts/exp/timeline.py).
 struct DChunkPlan {
   int64_t chunk_start[kMaxSegments + 1];            // prefix of per-segment chunk counts
+  int64_t chunk;                                    // tiles per claim (kDChunk; fewer for small inputs)
 };
 
 __device__ __forceinline__ uint32_t r16(uint64_t x) { return (uint32_t)((x + 15) & ~uint64_t(15)); }
@@ -475,8 +476,8 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
         const bool stage_gi = gsl >= 4;              // slice fits kGiSlots
         const int64_t seg_tiles = segs.tile_start[seg + 1] - segs.tile_start[seg];
         const int64_t zcap = pad128(H.zc);
-        const int64_t t0 = (c - cp.chunk_start[seg]) * kDChunk;
-        const int64_t t1 = (t0 + kDChunk < seg_tiles) ? t0 + kDChunk : seg_tiles;
+        const int64_t t0 = (c - cp.chunk_start[seg]) * cp.chunk;
+        const int64_t t1 = (t0 + cp.chunk < seg_tiles) ? t0 + cp.chunk : seg_tiles;
         // escape-range bounds of the chunk's tiles: bound(t) = gi[first group of t]
         const int64_t tb = t0 + lane;
         uint32_t bnd = 0;
@@ -906,9 +907,13 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
     }
   }
   DChunkPlan cp{};
+  // inputs of at most one tile per CTA are spread one tile per CTA (a 1 MiB
+  // message: 128 CTAs instead of 32; 26.8 against 30.3 us per codec step)
+  const int64_t all_tiles = segs.tile_start[segs.nseg];
+  cp.chunk = all_tiles <= cap2 ? 1 : kDChunk;
   for (int s = 0; s < segs.nseg; ++s) {
     const int64_t tiles = segs.tile_start[s + 1] - segs.tile_start[s];
-    cp.chunk_start[s + 1] = cp.chunk_start[s] + (tiles + kDChunk - 1) / kDChunk;
+    cp.chunk_start[s + 1] = cp.chunk_start[s] + (tiles + cp.chunk - 1) / cp.chunk;
   }
   const int64_t nchunks = cp.chunk_start[segs.nseg];
   const unsigned grid = (unsigned)(nchunks < cap2 ? nchunks : cap2);
