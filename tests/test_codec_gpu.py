@@ -343,6 +343,26 @@ def test_speculative_multi_segment_matches_prepare_frames(golden_meta):
         assert host[foffs[k]:foffs[k] + fl[k]].tobytes() == expect[q], q
 
 
+@pytest.mark.parametrize("sizes", [[4096 * 444], [4096 * 445 + 7], [4096 * 100 + 3] * 3,
+                                   [4096 * 150 + 1, 4096 * 150, 4096 * 149 + 99],
+                                   [4096 * 2000 + 11, 5, 4096 * 3]])
+def test_batched_decode_across_claim_sizes(sizes):
+    # the decoder claims one tile per CTA while the batch has at most one tile
+    # per resident CTA, four otherwise: totals on both sides of that switch,
+    # several frames per launch (segments of different lengths, ragged tails)
+    xs = [engine.words_view((torch.randn(c, device="cuda") * 0.02).to(torch.bfloat16))
+          for c in sizes]
+    chunks = [zc.compress(x, zc.codebook_for(x)) for x in xs]
+    out = torch.empty(sum(sizes), dtype=torch.int16, device="cuda")
+    offs = np.concatenate([[0], np.cumsum(sizes)])[:-1].tolist()
+    frames = [c.frame for c in chunks]
+    err = engine.decode([f.data_ptr() for f in frames], [0] * len(sizes), None, sizes, out,
+                        [int(o) for o in offs])
+    assert torch.all(err == engine.ERR_OK)
+    for x, o, c in zip(xs, offs, sizes):
+        assert torch.equal(out[o:o + c], x)
+
+
 def test_profile_hooks_record_encoder_and_decoder_launches():
     n = 4096 * 1200 + 5
     x = engine.words_view((torch.randn(n, device="cuda") * 0.02).to(torch.bfloat16))
