@@ -255,6 +255,7 @@ def run_ours(args):
     n = words.numel()
     stream = torch.cuda.current_stream()
 
+    whole_step = None
     if world == 1:
         frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device=dev)
         out = torch.empty(n, dtype=torch.int16, device=dev)
@@ -273,8 +274,7 @@ def run_ours(args):
         eager_enc, eager_dec = run_enc, run_dec
         if not args.no_graph:
             # captured once as CUDA graphs and replayed: no host launch overhead
-            # or event gaps between the kernels, identical kernels; events are
-            # recorded between the replays.  The per-kernel durations come from
+            # or event gaps between the kernels, identical kernels.  The per-kernel durations come from
             # an eager pass of the same steps right after the timed region.
             run_enc()
             run_dec()
@@ -284,6 +284,13 @@ def run_ours(args):
                 run_enc()
             with torch.cuda.graph(g_dec):
                 run_dec()
+            # the timed steps replay one graph per step (encode then decode);
+            # the two legs are timed afterwards from per-leg replays
+            g_step = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_step):
+                run_enc()
+                run_dec()
+            whole_step = g_step.replay
             run_enc, run_dec = g_enc.replay, g_dec.replay   # noqa: F811
 
         def step(rec=False):
@@ -346,10 +353,19 @@ def run_ours(args):
         if profiling:
             engine.profile_enable(True)    # events around each encoder / decoder launch
         t0.record(stream)
-        for _ in range(args.steps):
-            step(rec=(world == 1))
+        if whole_step is not None:
+            for _ in range(args.steps):
+                whole_step()
+        else:
+            for _ in range(args.steps):
+                step(rec=(world == 1))
         t1.record(stream)
         torch.cuda.synchronize()
+        if whole_step is not None:
+            # leg durations: per-leg graph replays with events between them
+            for _ in range(args.steps):
+                step(rec=True)
+            torch.cuda.synchronize()
         if world == 1 and not profiling:
             # per-kernel durations: the same steps launched eagerly with the
             # library's event hooks (kernel durations do not depend on how the
