@@ -309,8 +309,9 @@ def run_ours(args):
         # guess (1/128 sample), encoder pass 1 with the fused statistic and
         # certificate, run fix-up, then exact-statistic / re-encode pass 1 /
         # re-encode fix-up launches that return at once when the certificate
-        # decided and the guess held, decode
-        launches_per_step = 7
+        # decided and the guess held, decoder init (error words + chunk
+        # counter), decode
+        launches_per_step = 8
     else:
         comm = coll.Communicator.from_process_group()
         comm.use_p2p = args.transport == "p2p"
@@ -319,9 +320,9 @@ def run_ours(args):
 
         def step(rec=False):
             return coll.zip_all_gather(comm, shard)
-        # codebook+encode leg (6, as at N=1) + batched decode; the peer-memory
+        # codebook+encode leg (6, as at N=1) + decoder init + batched decode; the peer-memory
         # path adds wait-done, signal-ready, wait-ready, signal-done kernels
-        launches_per_step = 11 if comm.use_p2p else 7
+        launches_per_step = 12 if comm.use_p2p else 8
 
     # correctness gate before timing: bit-exact round trip
     err = step()
