@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-/* ABI version (1). */
+/* ABI version (2). */
 int zc_abi_version(void);
 /* Kernel timing hooks (measurement only).  zc_profile_enable(1) resets and
  * starts recording CUDA events on the launching stream around every pass-1

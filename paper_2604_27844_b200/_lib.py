@@ -56,6 +56,26 @@ EXPORTS = {
     "zc_free": (_int, [_vp]),
     "zc_signal_peers": (_int, [_P(_vp), _int, _int, ctypes.c_uint64, _vp]),
     "zc_wait_signals": (_int, [_vp, _int, _int, ctypes.c_uint64, ctypes.c_int64, _vp, _vp]),
+    # native collectives (csrc/zc_coll.cu)
+    "zc_nccl_id_bytes": (_int, []),
+    "zc_nccl_get_id": (_int, [_vp]),
+    "zc_comm_init": (_int, [_P(_vp), _vp, _int, _int, _i64, _int]),
+    "zc_comm_init_local": (_int, [_P(_vp), _int, _P(_int), _i64, _int]),
+    "zc_comm_destroy": (_int, [_vp]),
+    "zc_comm_abort": (_int, [_vp]),
+    "zc_comm_info": (_int, [_vp, _P(_int)]),
+    "zc_comm_last_error": (ctypes.c_char_p, [_vp, _P(_int)]),
+    "zc_comm_stats": (_int, [_vp, _P(ctypes.c_uint64), _P(ctypes.c_uint64)]),
+    "zc_comm_reserve": (_int, [_vp, _i64, _vp]),
+    "zc_allgather": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _int, _vp]),
+    "zc_allgather_raw": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "zc_alltoall": (_int, [_vp, _vp, _P(_i64), _P(_i64), _vp, _vp, _vp, _int, _vp]),
+    "zc_alltoall_raw": (_int, [_vp, _vp, _P(_i64), _P(_i64), _vp, _int, _vp]),
+    "zc_reduce_scatter": (_int, [_vp, _vp, _i64, _vp, _int, _vp, _vp, _int, _vp]),
+    "zc_reduce_scatter_raw": (_int, [_vp, _vp, _i64, _vp, _int, _vp, _vp]),
+    "zc_reduce_frames": (_int, [_vp, _int, _i64, _vp, _int, _vp, _vp, _vp]),
+    "zc_reduce_scratch_bytes": (_i64, [_int]),
+    "zc_red_src_bytes": (_int, []),
 }
 
 

@@ -17,7 +17,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libzipccl_b200.so"
-SOURCES = ["zc_abi.cu", "zc_encode.cu", "zc_decode.cu", "zc_stats.cu", "zc_p2p.cu"]
+SOURCES = ["zc_abi.cu", "zc_encode.cu", "zc_decode.cu", "zc_stats.cu", "zc_p2p.cu",
+           "zc_reduce.cu", "zc_coll.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -26,6 +27,21 @@ def nvcc() -> str:
         if cand and Path(cand).exists():
             return cand
     raise RuntimeError("nvcc not found")
+
+
+def nccl_paths():
+    """Headers + library of the NCCL torch loads (pip nvidia-nccl), so the
+    collective C-ABI links against the same libnccl.so.2 soname that torch
+    has already mapped; the system copy otherwise."""
+    import sysconfig
+    for base in (sysconfig.get_paths()["purelib"], sysconfig.get_paths()["platlib"]):
+        d = Path(base) / "nvidia" / "nccl"
+        if (d / "include" / "nccl.h").exists() and (d / "lib" / "libnccl.so.2").exists():
+            return str(d / "include"), str(d / "lib")
+    for inc, lib in (("/usr/include", "/usr/lib/x86_64-linux-gnu"),):
+        if Path(inc, "nccl.h").exists():
+            return inc, lib
+    raise RuntimeError("nccl.h not found")
 
 
 def needs_build() -> bool:
@@ -40,8 +56,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
     srcs = [str(CSRC / s) for s in SOURCES if (CSRC / s).exists()]
+    inc, libdir = nccl_paths()
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-           "-shared", "-o", str(LIB) + ".tmp", *srcs]
+           "-I", inc, "-shared", "-o", str(LIB) + ".tmp", *srcs,
+           "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libdir}", "-lpthread"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

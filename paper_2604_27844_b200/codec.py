@@ -473,6 +473,17 @@ def decompress(chunk: CompressedChunk, out: torch.Tensor | None = None) -> torch
     invariants are re-checked on the device first, as in the reference."""
     chunk.check_structure()
     if out is not None:
+        if not isinstance(out, torch.Tensor) or out.element_size() != 2 or \
+                out.dtype.is_complex:
+            raise ValueError("decompress: out must be a 16-bit tensor")
+        if not out.is_contiguous():
+            raise ValueError("decompress: out must be contiguous (it is written in place)")
+        if out.device != chunk.frame.device:
+            raise ValueError(f"decompress: out is on {out.device}, the frame on "
+                             f"{chunk.frame.device}")
+        if out.numel() < chunk.element_count:
+            raise ValueError(f"decompress: out holds {out.numel()} elements, the chunk "
+                             f"{chunk.element_count}")
         out = engine.words_view(out)
     return _run_decode(chunk, True, CorruptChunkError, out)
 

@@ -2,26 +2,28 @@
 
 Same semantics as the reference (outputs bit-identical to the uncompressed
 collectives, rank-order results, same exception classes), with the element
-work on the GPU and the frames moving over the communicator's device byte
-movers (NCCL over NVLink for a ``DistCommunicator``):
+work on the GPU.  Two implementations of the same protocols:
 
-* ``zip_all_gather``: codebook (K1) + encode (K2) of the local shard; the
-  static section has the same size on every rank (a function of n alone),
-  so it moves with one all-gather posted right after the encoder; the frame
-  lengths are gathered on the side and the variable dynamic sections follow
-  in one padded all-gather; every peer frame is decoded by ONE batched K3
-  launch straight into the output (reference collectives.py:203-227).
+* native (``comm.native`` set: NCCL process groups and thread ranks): the
+  C++ engine of csrc/zc_coll.cu (see native.py) -- the peer-memory plane
+  (the decoder pulls every peer's frame over NVLink as soon as that peer
+  published it; no host round trip) or the message plane (the reference's
+  size phase / design-1 / design-2 protocols over NCCL);
+* generic (any ``Communicator`` byte movers: gloo, or thread ranks with
+  ``native=False``): the same protocols driven from Python.
+
+* ``zip_all_gather``: codebook (K1) + encode (K2) of the local shard, the
+  reference's size phase (8 B per peer), frames, ONE batched decode (K3)
+  straight into the output (reference collectives.py:203-227).
 * ``zip_all_to_all_d1`` / ``_d2``: one codebook over the non-self, non-empty
   chunks (collectives.py:230-242), all peer frames encoded by ONE batched K4
-  launch into one send buffer, then design 1 (metadata, whole frames) or
-  design 2 (static sections pre-sized from recv_counts, dynamic sizes,
-  dynamic sections) over grouped send/recv; one batched decode launch.
+  launch; design 1 = 16 B of metadata per peer then frames, design 2 =
+  static sections pre-sized from recv_counts with no metadata, then 8 B
+  dynamic sizes, then dynamic sections (collectives.py:245-325) -- the
+  reference's wire accounting (d1 - d2 = 8 B per peer).
 * ``zip_reduce_scatter`` / ``zip_all_reduce``: design-2
-  all-to-all then the reference's float32 reduction in ascending rank order
-  and RNE narrowing with its NaN rule.
-
-Counts are agreed before any device transfer (NCCL needs matching sizes),
-which costs 8 B per peer on top of the reference's metadata.
+  all-to-all then ONE fused decode + float32 reduction in ascending rank
+  order with the reference's RNE narrowing and NaN rule (zc_reduce.cu).
 """
 
 from __future__ import annotations
@@ -69,8 +71,25 @@ def _pack(chunks, device):
     words = [device_words(c, device) for c in chunks]
     counts = [w.numel() for w in words]
     offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    buf = torch.cat(words) if sum(counts) else torch.empty(0, dtype=torch.int16, device=device)
-    return buf, [int(o) for o in offs[:-1]], counts
+    if not sum(counts):
+        return torch.empty(0, dtype=torch.int16, device=device), [int(o) for o in offs[:-1]], counts
+    live = [w for w in words if w.numel()]
+    base = live[0]
+    consecutive = all(w.untyped_storage().data_ptr() == base.untyped_storage().data_ptr()
+                      for w in live) and all(
+        a.data_ptr() + 2 * a.numel() == b.data_ptr() for a, b in zip(live, live[1:]))
+    if consecutive:   # views of one send buffer (MoE dispatch): no copy
+        start = base.storage_offset()
+        flat = base.new_empty(0).set_(base.untyped_storage(), start, (int(offs[-1]),), (1,))
+        return flat, [int(o) for o in offs[:-1]], counts
+    return torch.cat(words), [int(o) for o in offs[:-1]], counts
+
+
+def _native(comm: Communicator):
+    """The communicator's native engine, or None for the generic path."""
+    if not getattr(comm, "use_native", True):
+        return None
+    return getattr(comm, "native", None)
 
 
 def _raise_decode_errors(err: torch.Tensor, peers: list) -> None:
@@ -87,10 +106,22 @@ def _raise_decode_errors(err: torch.Tensor, peers: list) -> None:
 # reference (uncompressed) collectives: the oracles and the switcher's raw path
 
 def reference_all_gather(comm: Communicator, local) -> torch.Tensor:
-    """Raw all-gather (collectives.py:97-111): NCCL all_gather on device."""
+    """Raw all-gather (collectives.py:97-111): element counts agreed (once
+    per shape on NCCL communicators), then ncclAllGather / device copies."""
     words = device_words(local, _dev(comm))
     if comm.world_size == 1:
         return words.clone()
+    native = _native(comm)
+    if native is not None:
+        agreed = comm.__dict__.setdefault("_agreed_ag", set())
+        if words.numel() not in agreed or native.check_counts:
+            counts = comm.allgather_ints(words.numel())
+            for p, c in enumerate(counts):
+                if c != words.numel():
+                    raise ProtocolError(f"all-gather element count mismatch: rank {comm.rank} "
+                                        f"has {words.numel()}, rank {p} declared {c}")
+            agreed.add(words.numel())
+        return native.all_gather_raw(words)
     counts = comm.allgather_ints(words.numel())
     for p, c in enumerate(counts):
         if c != words.numel():
@@ -108,6 +139,13 @@ def reference_all_to_all(comm: Communicator, spec: AlltoAllSpec) -> list:
     if comm.world_size == 1:
         return [device_words(spec.send_chunks[0], dev).clone()]
     buf, offs, counts = _pack(spec.send_chunks, dev)
+    native = _native(comm)
+    if native is not None:
+        saved, native.check_counts = native.check_counts, True   # the reference's size phase
+        try:
+            return native.all_to_all_raw(buf, counts, spec.recv_counts)
+        finally:
+            native.check_counts = saved
     declared = comm.exchange_sizes(counts)
     for p in comm.peers():
         if declared[p] != spec.recv_counts[p]:
@@ -122,13 +160,14 @@ def reference_all_to_all(comm: Communicator, spec: AlltoAllSpec) -> list:
 
 
 def _reduce_chunks(chunks: list, output: str) -> torch.Tensor:
-    """float32 sum in list (= ascending rank) order (collectives.py:137-144)."""
-    acc = bf16.to_float32(chunks[0]).clone()
-    for c in chunks[1:]:
-        acc += bf16.to_float32(c)
-    if output == "fp32":
-        return acc
-    return bf16.from_float32(acc)
+    """float32 sum in list (= ascending rank) order (collectives.py:137-144)
+    with numpy's NaN propagation and the reference's RNE narrowing: one
+    launch of the fused reduce kernel over raw word sources."""
+    from .native import reduce_sources
+    n = chunks[0].numel()
+    out, _, _ = reduce_sources([("raw", c.contiguous()) for c in chunks], n, output,
+                               chunks[0].device)
+    return out
 
 
 def _split_shards(comm: Communicator, local) -> list:
@@ -141,9 +180,14 @@ def _split_shards(comm: Communicator, local) -> list:
 
 
 def reference_reduce_scatter(comm: Communicator, local, output: str = "bf16") -> torch.Tensor:
+    """Raw all-to-all of the shards + the float32 reduction (collectives.py:147-170)."""
     shards = _split_shards(comm, local)
     if comm.world_size == 1:
         return _reduce_chunks(shards, output)
+    native = _native(comm)
+    if native is not None:
+        _agree_shard(comm, shards[0].numel())
+        return native.reduce_scatter(device_words(local, _dev(comm)), None, output, raw=True)
     spec = AlltoAllSpec(shards, [shards[0].numel()] * comm.world_size)
     return _reduce_chunks(reference_all_to_all(comm, spec), output)
 
@@ -151,62 +195,59 @@ def reference_reduce_scatter(comm: Communicator, local, output: str = "bf16") ->
 # ---------------------------------------------------------------------------
 # compressed collectives
 
-def zip_all_gather(comm: Communicator, local, sigma: float | None = None,
-                   _return_device: bool = True) -> torch.Tensor:
+def zip_all_gather(comm: Communicator, local, sigma: float | None = None) -> torch.Tensor:
     """All-gather with compressed payloads, bit-identical to the reference
-    all-gather (collectives.py:203-227)."""
-    if getattr(comm, "use_p2p", False):
-        return zip_all_gather_p2p(comm, local, sigma)
+    all-gather (collectives.py:203-227).
+
+    Over a generic communicator (thread hub, gloo): K1+K2 encode the local
+    shard into one frame; ONE exchange carries (element count, frame bytes)
+    per rank -- the reference's size phase (8 B/peer of frame length) plus
+    the count the reference checks when it parses the peer frame; the static
+    sections (equal size, a function of n) move in one all-gather, the
+    dynamic sections point to point at their exact sizes; ONE batched K3
+    launch decodes every peer frame into the output."""
     dev = _dev(comm)
     words = device_words(local, dev)
     n = words.numel()
     W = comm.world_size
     if W == 1:
         return words.clone()
-    counts = comm.allgather_ints(n)
+    native = _native(comm)
+    if native is not None and n > 0:
+        return native.all_gather(words, sigma)
     if n == 0:
-        for p, c in enumerate(counts):
+        rows = comm.allgather_vec([0, 0])
+        comm._count(8 * (W - 1), W - 1)
+        for p, (c, _) in enumerate(rows):
             if c != 0:
                 raise ProtocolError(f"all-gather frame size mismatch: rank {comm.rank} has 0, "
                                     f"rank {p} declared {c}")
         return torch.empty(0, dtype=torch.int16, device=dev)
-    for p, c in enumerate(counts):
+    S = engine.static_bytes(n, GS_LOG2)
+    frame = torch.empty(engine.max_frame_bytes(n, GS_LOG2), dtype=torch.uint8, device=dev)
+    _, flen = codec.device_encode(words, [(0, n)], sigma, frame, [0], GS_LOG2)
+    rows = comm.allgather_vec([n, int(flen.item())])
+    comm._count(8 * (W - 1), W - 1)
+    for p, (c, _) in enumerate(rows):
         if c != n:
             raise CollectiveError(f"frame holds {c} elements, expected {n}", peer=p)
-    # K1 + K2: codebook from the local shard, one frame
-    S = engine.static_bytes(n, GS_LOG2)
-    cap = engine.max_frame_bytes(n, GS_LOG2)
-    frame = torch.empty(cap, dtype=torch.uint8, device=dev)
-    _, flen = codec.device_encode(words, [(0, n)], sigma, frame, [0], GS_LOG2)
-    # frame lengths first (tiny), then the static sections (size known from n)
-    lens = torch.empty(W, dtype=torch.int64, device=dev)
-    if isinstance(comm, DistCommunicator) and comm.on_device:
-        # NCCL runs both gathers in order on its stream: waiting on the tiny
-        # length gather lets the host learn the dynamic sizes while the static
-        # sections are still in flight (design-2 overlap, SURVEY §7 step 8)
-        import torch.distributed as dist
-        h = dist.all_gather_into_tensor(lens, flen, group=comm.group, async_op=True)
-        static = torch.empty(W * S, dtype=torch.uint8, device=dev)
-        hs = dist.all_gather_into_tensor(static, frame[:S], group=comm.group, async_op=True)
-        h.wait()
-        dyn_lens = [int(v) - S for v in lens.cpu().tolist()]
-        hs.wait()
-        comm._count((8 + S) * (W - 1), 2 * (W - 1))
-    else:
-        dyn_lens = [v - S for v in comm.allgather_ints(int(flen.item()))]
-        static = torch.empty(W * S, dtype=torch.uint8, device=dev)
-        comm.all_gather_bytes(frame[:S], static)
-    dmax = max(dyn_lens)
-    dyn = torch.empty(max(W * dmax, 1), dtype=torch.uint8, device=dev)
-    if dmax:
-        comm.all_gather_bytes(frame[S:S + dmax], dyn[:W * dmax])
+    dyn_lens = [fl - S for _, fl in rows]
+    static = torch.empty(W * S, dtype=torch.uint8, device=dev)
+    comm.all_gather_bytes(frame[:S], static)
+    dyn = torch.empty(max(sum(dyn_lens), 1), dtype=torch.uint8, device=dev)
+    doff = np.concatenate([[0], np.cumsum(dyn_lens)]).astype(np.int64)
+    me = comm.rank
+    own = frame[S:S + dyn_lens[me]]
+    comm.sendrecv_bytes({p: own for p in comm.peers()},
+                        {p: dyn[int(doff[p]):int(doff[p + 1])] for p in comm.peers()},
+                        label="dynamic section")
     out = torch.empty(W * n, dtype=torch.int16, device=dev)
     peers = comm.peers()
     err = engine.decode([static.data_ptr() + p * S for p in peers],
-                        [dyn.data_ptr() + p * dmax for p in peers],
+                        [dyn.data_ptr() + int(doff[p]) for p in peers],
                         [dyn_lens[p] for p in peers], [n] * len(peers), out,
                         [p * n for p in peers])
-    out[comm.rank * n:(comm.rank + 1) * n].copy_(words)
+    out[me * n:(me + 1) * n].copy_(words)
     _raise_decode_errors(err, peers)
     return out
 
@@ -268,20 +309,34 @@ def _agree_counts(comm: Communicator, spec: AlltoAllSpec, counts, what: str):
 def zip_all_to_all_d1(comm: Communicator, spec: AlltoAllSpec,
                       sigma: float | None = None) -> list:
     """Design 1 (collectives.py:245-278): metadata (count, frame bytes) per
-    peer, then whole frames, then decode."""
+    peer -- 16 B, as two u64 exchanges -- then whole frames, then one batched
+    decode."""
     _check_world(comm, spec.world_size)
     dev = _dev(comm)
     if comm.world_size == 1:
         return [device_words(spec.send_chunks[0], dev).clone()]
     buf, offs, counts = _pack(spec.send_chunks, dev)
+    native = _native(comm)
+    if native is not None:
+        return native.all_to_all(buf, counts, spec.recv_counts, sigma, design=1)
     _agree_counts(comm, spec, counts, "count")
     frames, frame_off, frame_len = _prepare_frames(comm, buf, offs, counts, sigma)
     got_len = comm.exchange_sizes(frame_len)
+    for p in comm.peers():
+        want = spec.recv_counts[p]
+        if want == 0:
+            if got_len[p]:
+                raise CollectiveError(f"expected an empty frame, got {got_len[p]} bytes", peer=p)
+            continue
+        s = codec.static_size_bytes(want)
+        if got_len[p] < s or got_len[p] % 128:
+            raise CollectiveError(f"frame length {got_len[p]} cannot hold {want} elements",
+                                  peer=p)
     recv_bufs = {p: torch.empty(got_len[p], dtype=torch.uint8, device=dev)
                  for p in comm.peers() if spec.recv_counts[p]}
     sends = {p: frames[frame_off[p]:frame_off[p] + frame_len[p]]
              for p in comm.peers() if frame_len[p]}
-    comm.sendrecv_bytes(sends, recv_bufs)
+    comm.sendrecv_bytes(sends, recv_bufs, label="frame")
     peers_in = sorted(recv_bufs)
     return _finish_a2a(comm, spec, buf, offs, counts, recv_bufs, peers_in,
                        [recv_bufs[p].data_ptr() for p in peers_in], [0] * len(peers_in),
@@ -291,18 +346,25 @@ def zip_all_to_all_d1(comm: Communicator, spec: AlltoAllSpec,
 
 def zip_all_to_all_d2(comm: Communicator, spec: AlltoAllSpec,
                       sigma: float | None = None) -> list:
-    """Design 2 (collectives.py:281-325): static sections first (receivers
-    pre-size them from recv_counts), then dynamic sizes, then dynamic
-    sections; frames are decoded from the split receive buffers in place.
-    With ``comm.use_p2p`` the peer-memory pull-decode path is used instead."""
-    if getattr(comm, "use_p2p", False):
-        return zip_all_to_all_p2p(comm, spec, sigma)
+    """Design 2 (collectives.py:281-325): static sections first, receives
+    pre-sized from recv_counts with NO metadata (the property design 2
+    exists for), then the u64 dynamic sizes (8 B/peer),
+    then the dynamic sections; frames are decoded from the split receive
+    buffers in place.  A sender whose count disagrees with the receiver's
+    expectation is caught by the transport's size check (thread hub:
+    ProtocolError "static section ...") or by the frame header
+    (CollectiveError); ``comm.check_counts = True`` adds an explicit count
+    agreement first, for transports that cannot see mismatched sizes."""
     _check_world(comm, spec.world_size)
     dev = _dev(comm)
     if comm.world_size == 1:
         return [device_words(spec.send_chunks[0], dev).clone()]
     buf, offs, counts = _pack(spec.send_chunks, dev)
-    _agree_counts(comm, spec, counts, "static")
+    native = _native(comm)
+    if native is not None:
+        return native.all_to_all(buf, counts, spec.recv_counts, sigma, design=2)
+    if getattr(comm, "check_counts", False):
+        _agree_counts(comm, spec, counts, "static")
     frames, frame_off, frame_len = _prepare_frames(comm, buf, offs, counts, sigma)
     peers_out = [p for p in comm.peers() if frame_len[p]]
     peers_in = [p for p in comm.peers() if spec.recv_counts[p]]
@@ -310,26 +372,53 @@ def zip_all_to_all_d2(comm: Communicator, spec: AlltoAllSpec,
     s_in = {p: codec.static_size_bytes(spec.recv_counts[p]) for p in peers_in}
     statics = {p: torch.empty(s_in[p], dtype=torch.uint8, device=dev) for p in peers_in}
     comm.sendrecv_bytes({p: frames[frame_off[p]:frame_off[p] + s_out[p]] for p in peers_out},
-                        statics)
+                        statics, label="static section")
     dyn_len = [frame_len[p] - s_out[p] if p in s_out else 0 for p in range(comm.world_size)]
     got_dyn = comm.exchange_sizes(dyn_len)
-    dyns = {p: torch.empty(max(got_dyn[p], 0), dtype=torch.uint8, device=dev) for p in peers_in}
+    for p in peers_in:
+        if got_dyn[p] % 128:
+            raise CollectiveError(f"dynamic section of {got_dyn[p]} bytes is not 128-aligned",
+                                  peer=p)
+    dyns = {p: torch.empty(got_dyn[p], dtype=torch.uint8, device=dev)
+            for p in peers_in if got_dyn[p]}
     comm.sendrecv_bytes({p: frames[frame_off[p] + s_out[p]:frame_off[p] + frame_len[p]]
-                         for p in peers_out}, dyns)
+                         for p in peers_out if dyn_len[p]}, dyns, label="dynamic section")
     return _finish_a2a(comm, spec, buf, offs, counts, None, peers_in,
                        [statics[p].data_ptr() for p in peers_in],
-                       [dyns[p].data_ptr() if dyns[p].numel() else statics[p].data_ptr()
+                       [dyns[p].data_ptr() if p in dyns else statics[p].data_ptr()
                         for p in peers_in],
                        [got_dyn[p] for p in peers_in])
+
+
+def _agree_shard(comm: Communicator, shard: int) -> None:
+    """Reduce-scatter shard lengths agree (reference _agree_u64,
+    collectives.py:83-90, :153); once per shape on native communicators."""
+    agreed = comm.__dict__.setdefault("_agreed_rs", set())
+    if shard in agreed:
+        return
+    for p, c in enumerate(comm.allgather_ints(shard)):
+        if c != shard:
+            raise ProtocolError(f"reduce-scatter shard length mismatch: rank {comm.rank} has "
+                                f"{shard}, rank {p} declared {c}")
+    agreed.add(shard)
 
 
 def zip_reduce_scatter(comm: Communicator, local, sigma: float | None = None,
                        output: str = "bf16") -> torch.Tensor:
     """Compressed all-to-all (design 2) + float32 reduction in ascending rank
-    order (collectives.py:328-341)."""
+    order (collectives.py:328-341): on native communicators one fused decode
+    + reduce kernel consumes the peers' frames (over NVLink on the
+    peer-memory plane) and the self shard."""
     shards = _split_shards(comm, local)
     if comm.world_size == 1:
         return _reduce_chunks(shards, output)
+    native = _native(comm)
+    if native is not None:
+        if shards[0].numel() == 0:
+            return torch.empty(0, dtype=torch.float32 if output == "fp32" else torch.int16,
+                               device=_dev(comm))
+        _agree_shard(comm, shards[0].numel())
+        return native.reduce_scatter(device_words(local, _dev(comm)), sigma, output)
     spec = AlltoAllSpec(shards, [shards[0].numel()] * comm.world_size)
     return _reduce_chunks(zip_all_to_all_d2(comm, spec, sigma), output)
 
@@ -365,124 +454,3 @@ def timed_call(comm: Communicator, fn):
         torch.cuda.current_stream().synchronize()
     elapsed = comm.now() - start
     return result, max(allgather_scalar(comm, elapsed))
-
-
-# ---------------------------------------------------------------------------
-# peer-memory (NVLink) pull-decode variants — SURVEY K5 "fused pull-decode"
-
-def _use_p2p(comm: Communicator) -> bool:
-    return bool(getattr(comm, "use_p2p", isinstance(comm, HubCommunicator)))
-
-
-def zip_all_gather_p2p(comm: Communicator, local, sigma: float | None = None) -> torch.Tensor:
-    """All-gather where the transfer IS the decode: every rank encodes its
-    shard into its own symmetric buffer, signals its peers device-side, and
-    each rank's decoder pulls the peer frames over NVLink (TMA from peer HBM)
-    straight into the gathered output.  Bit-identical to reference_all_gather."""
-    from .peer import workspace_for
-    dev = _dev(comm)
-    words = device_words(local, dev)
-    n = words.numel()
-    W = comm.world_size
-    if W == 1:
-        return words.clone()
-    counts = comm.allgather_ints(n)
-    if n == 0:
-        for p, c in enumerate(counts):
-            if c != 0:
-                raise ProtocolError(f"all-gather frame size mismatch: rank {comm.rank} has 0, "
-                                    f"rank {p} declared {c}")
-        return torch.empty(0, dtype=torch.int16, device=dev)
-    for p, c in enumerate(counts):
-        if c != n:
-            raise CollectiveError(f"frame holds {c} elements, expected {n}", peer=p)
-    ws = workspace_for(comm, engine.max_frame_bytes(max(counts), GS_LOG2))
-    e = ws.epoch + 1
-    ws.epoch = e
-    werr = torch.full((1,), engine.ERR_OK, dtype=torch.int32, device=dev)
-    if e > 1:
-        ws.wait(1, e - 1, werr)                 # peers finished reading my last frame
-    _, flen = codec.device_encode(words, [(0, n)], sigma, ws.buf, [256], GS_LOG2)
-    ws.signal(0, e)                             # my frame is ready
-    ws.wait(0, e, werr)                         # every peer's frame is ready
-    out = torch.empty(W * n, dtype=torch.int16, device=dev)
-    peers = comm.peers()
-    err = engine.decode([ws.peer_base[p] + 256 for p in peers], [0] * len(peers), None,
-                        [n] * len(peers), out, [p * n for p in peers])
-    ws.signal(1, e)                             # done reading the peers' frames
-    out[comm.rank * n:(comm.rank + 1) * n].copy_(words)
-    del flen
-    if int(werr.item()) != engine.ERR_OK:
-        raise CollectiveError("peer frame never became ready (timeout)")
-    _raise_decode_errors(err, peers)
-    return out
-
-
-def _a2a_layout(counts_row: list, sender: int) -> list:
-    """Frame offsets inside `sender`'s symmetric buffer: peers in rank order,
-    capacity max_frame_bytes(count) each (a pure function of the counts, so
-    every rank derives every sender's layout without exchanging offsets)."""
-    offs, pos = [0] * len(counts_row), 0
-    for q, c in enumerate(counts_row):
-        offs[q] = pos
-        if q != sender and c:
-            pos += engine.max_frame_bytes(c, GS_LOG2)
-    return offs + [pos]
-
-
-def zip_all_to_all_p2p(comm: Communicator, spec: AlltoAllSpec,
-                       sigma: float | None = None) -> list:
-    """All-to-all where the transfer IS the decode (MoE dispatch/combine):
-    one batched K4 launch encodes every peer frame into this rank's symmetric
-    buffer, peers are signalled device-side, and one batched K3 launch pulls
-    this rank's frame from every peer's HBM over NVLink and decodes it in
-    place.  Results identical to reference_all_to_all."""
-    from .peer import workspace_for
-    _check_world(comm, spec.world_size)
-    dev = _dev(comm)
-    W, me = comm.world_size, comm.rank
-    if W == 1:
-        return [device_words(spec.send_chunks[0], dev).clone()]
-    buf, offs, counts = _pack(spec.send_chunks, dev)
-    # the full count matrix: protocol check + every sender's layout
-    if isinstance(comm, HubCommunicator):
-        matrix = comm._post_and_collect(list(counts))
-    else:
-        import torch.distributed as dist
-        rows = [None] * W
-        dist.all_gather_object(rows, list(counts), group=comm.group)
-        matrix = rows
-    for p in comm.peers():
-        if matrix[p][me] != spec.recv_counts[p]:
-            raise ProtocolError(f"rank {p} will send {matrix[p][me]} elements, "
-                                f"rank {me} expected {spec.recv_counts[p]}")
-    layouts = [_a2a_layout(matrix[p], p) for p in range(W)]
-    ws = workspace_for(comm, max(lay[-1] for lay in layouts) + 128)
-    e = ws.epoch + 1
-    ws.epoch = e
-    werr = torch.full((1,), engine.ERR_OK, dtype=torch.int32, device=dev)
-    if e > 1:
-        ws.wait(1, e - 1, werr)
-    peers_out = [q for q in comm.peers() if counts[q]]
-    if peers_out:
-        segs = [(offs[q], counts[q]) for q in peers_out]
-        codec.device_encode(buf, segs, sigma, ws.buf, [256 + layouts[me][q] for q in peers_out],
-                            GS_LOG2)
-    ws.signal(0, e)
-    ws.wait(0, e, werr)
-    peers_in = [p for p in comm.peers() if spec.recv_counts[p]]
-    roffs = np.concatenate([[0], np.cumsum(spec.recv_counts)]).astype(np.int64)
-    flat = torch.empty(max(int(roffs[-1]), 1), dtype=torch.int16, device=dev)
-    err = None
-    if peers_in:
-        err = engine.decode([ws.peer_base[p] + 256 + layouts[p][me] for p in peers_in],
-                            [0] * len(peers_in), None, [spec.recv_counts[p] for p in peers_in],
-                            flat, [int(roffs[p]) for p in peers_in])
-    ws.signal(1, e)
-    result = [flat[int(roffs[p]):int(roffs[p]) + spec.recv_counts[p]] for p in range(W)]
-    result[me] = buf[offs[me]:offs[me] + counts[me]].clone()
-    if int(werr.item()) != engine.ERR_OK:
-        raise CollectiveError("peer frame never became ready (timeout)")
-    if err is not None:
-        _raise_decode_errors(err, peers_in)
-    return result

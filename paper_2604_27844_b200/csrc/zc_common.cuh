@@ -25,6 +25,23 @@ constexpr int kEPT = 16;                    // elements per thread (two 16-B loa
 constexpr int kTile = kThreads * kEPT;      // 4096 elements per tile
 constexpr int kWarps = kThreads / 32;
 
+// Per-device cache of a host-side launch setting (occupancy caps; the
+// MaxDynamicSharedMemorySize attribute is also set per device inside `init`).
+// Thread ranks may drive several GPUs from one process.
+constexpr int kMaxDevices = 64;
+template <class F>
+inline int per_device(int (&slot)[kMaxDevices], F init) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return init();
+  int v = __atomic_load_n(&slot[dev], __ATOMIC_ACQUIRE);
+  if (v == 0) {
+    v = init();
+    __atomic_store_n(&slot[dev], v, __ATOMIC_RELEASE);
+  }
+  return v;
+}
+
 ZC_HD int64_t pad128(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
@@ -68,6 +85,8 @@ enum Err : int32_t {
   kErrZeroCount = 18,
   kErrCountMismatch = 19,   // collectives: header element_count != expected
   kErrTimeout = 20,         // p2p: peer never signalled
+  kErrGroupTooLarge = 21,   // ring decoder: gs > one tile (decode with large_groups)
+  kErrGroupSize = 22,       // collectives' fused reduce: frames use 512-element groups
 };
 
 // ---- memory-ordering helpers (decoupled look-back, peer flags) -------------
@@ -298,7 +317,75 @@ struct DecodeSegs {
   int64_t dyn_len[kMaxSegments];          // bytes available in dyn (-1 unknown)
   int64_t n[kMaxSegments];                // expected element count
   int64_t out_off[kMaxSegments];          // element offset into out
+  // pull mode (peer frames decoded behind arrival, decode_ring_kernel<true>):
+  // segment s may be staged once *ready[s] >= epoch (null: ready now)
+  const uint64_t* ready[kMaxSegments];
+  uint64_t epoch;
+  int64_t timeout_ns;                     // 0: wait forever
 };
+
+struct HeaderInfo {
+  int64_t n, zc;
+  int gsl;
+  uint32_t tbl_lo, tbl_hi;   // PRMT decode table: byte c = entries[c-1], byte 0 = 0
+  int32_t err;
+};
+
+// Mirrors container.parse_header + parse offset/length checks, in order.
+__device__ __forceinline__ HeaderInfo check_header(const uint8_t* h, int64_t expect_n, int64_t dyn_len) {
+  HeaderInfo r{};
+  const uint64_t q0 = reinterpret_cast<const uint64_t*>(h)[0];
+  const uint64_t n = reinterpret_cast<const uint64_t*>(h)[1];
+  const uint64_t zc = reinterpret_cast<const uint64_t*>(h)[2];
+  const uint64_t q3 = reinterpret_cast<const uint64_t*>(h)[3];
+  const uint32_t* offs = reinterpret_cast<const uint32_t*>(h + 32);
+  const uint32_t magic = (uint32_t)q0;
+  const int version = (int)((q0 >> 32) & 0xFF), flags = (int)((q0 >> 40) & 0xFF);
+  const int gsl = (int)((q0 >> 48) & 0xFF);
+  r.err = kOk;
+  if (magic != 0x4C43435Au) { r.err = kErrMagic; return r; }   // "ZCCL"
+  if (version != 1) { r.err = kErrVersion; return r; }
+  if (flags != 0) { r.err = kErrFlags; return r; }
+  if (gsl > 30) { r.err = kErrGsLog2; return r; }
+  if (n < 1) { r.err = kErrElementCount; return r; }
+  if (zc > n) { r.err = kErrZeroCountHeader; return r; }
+  uint8_t e[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) e[i] = (uint8_t)(q3 >> (8 * i));
+  for (int i = 0; i < 7; ++i)
+    for (int j = i + 1; j < 7; ++j)
+      if (e[i] == e[j]) { r.err = kErrCodebookDistinct; return r; }
+  if (e[7] != e[0]) { r.err = kErrCodebookBase; return r; }
+  if (n > (uint64_t(1) << 40)) { r.err = kErrOffset0 + 1; return r; }
+  const Layout L = layout_of((int64_t)n, gsl);
+  for (int i = 0; i < 6; ++i)
+    if ((int64_t)offs[i] != L.off[i]) { r.err = kErrOffset0 + i; return r; }
+  if (dyn_len >= 0 && dyn_len != pad128((int64_t)zc)) { r.err = kErrFrameLength; return r; }
+  if (expect_n >= 0 && (int64_t)n != expect_n) { r.err = kErrCountMismatch; return r; }
+  r.n = (int64_t)n;
+  r.zc = (int64_t)zc;
+  r.gsl = gsl;
+  r.tbl_lo = (uint32_t)e[0] << 8 | (uint32_t)e[1] << 16 | (uint32_t)e[2] << 24;
+  r.tbl_hi = (uint32_t)e[3] | (uint32_t)e[4] << 8 | (uint32_t)e[5] << 16 | (uint32_t)e[6] << 24;
+  return r;
+}
+
+// One contribution to the fused reduce-scatter (zc_reduce.cu): a frame
+// (local, a split design-2 receive buffer, or a peer's HBM) or raw words.
+struct RedSrc {
+  const uint8_t* stat;     // frame start, or the raw words when raw != 0
+  const uint8_t* dyn;      // zero-exponent section (null: in place)
+  int64_t dyn_len;         // bytes in dyn (-1 unknown)
+  const uint64_t* ready;   // pull: wait until *ready >= epoch (null: ready)
+  int32_t raw;
+  int32_t pad;
+};
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Kernel timing hooks (zc_profile_enable / zc_profile_read in the C-ABI):
 // when enabled, CUDA events are recorded on the launching stream right

@@ -23,52 +23,6 @@
 
 namespace zc {
 
-struct HeaderInfo {
-  int64_t n, zc;
-  int gsl;
-  uint32_t tbl_lo, tbl_hi;   // PRMT decode table: byte c = entries[c-1], byte 0 = 0
-  int32_t err;
-};
-
-// Mirrors container.parse_header + parse offset/length checks, in order.
-__device__ HeaderInfo check_header(const uint8_t* h, int64_t expect_n, int64_t dyn_len) {
-  HeaderInfo r{};
-  const uint64_t q0 = reinterpret_cast<const uint64_t*>(h)[0];
-  const uint64_t n = reinterpret_cast<const uint64_t*>(h)[1];
-  const uint64_t zc = reinterpret_cast<const uint64_t*>(h)[2];
-  const uint64_t q3 = reinterpret_cast<const uint64_t*>(h)[3];
-  const uint32_t* offs = reinterpret_cast<const uint32_t*>(h + 32);
-  const uint32_t magic = (uint32_t)q0;
-  const int version = (int)((q0 >> 32) & 0xFF), flags = (int)((q0 >> 40) & 0xFF);
-  const int gsl = (int)((q0 >> 48) & 0xFF);
-  r.err = kOk;
-  if (magic != 0x4C43435Au) { r.err = kErrMagic; return r; }   // "ZCCL"
-  if (version != 1) { r.err = kErrVersion; return r; }
-  if (flags != 0) { r.err = kErrFlags; return r; }
-  if (gsl > 30) { r.err = kErrGsLog2; return r; }
-  if (n < 1) { r.err = kErrElementCount; return r; }
-  if (zc > n) { r.err = kErrZeroCountHeader; return r; }
-  uint8_t e[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) e[i] = (uint8_t)(q3 >> (8 * i));
-  for (int i = 0; i < 7; ++i)
-    for (int j = i + 1; j < 7; ++j)
-      if (e[i] == e[j]) { r.err = kErrCodebookDistinct; return r; }
-  if (e[7] != e[0]) { r.err = kErrCodebookBase; return r; }
-  if (n > (uint64_t(1) << 40)) { r.err = kErrOffset0 + 1; return r; }
-  const Layout L = layout_of((int64_t)n, gsl);
-  for (int i = 0; i < 6; ++i)
-    if ((int64_t)offs[i] != L.off[i]) { r.err = kErrOffset0 + i; return r; }
-  if (dyn_len >= 0 && dyn_len != pad128((int64_t)zc)) { r.err = kErrFrameLength; return r; }
-  if (expect_n >= 0 && (int64_t)n != expect_n) { r.err = kErrCountMismatch; return r; }
-  r.n = (int64_t)n;
-  r.zc = (int64_t)zc;
-  r.gsl = gsl;
-  r.tbl_lo = (uint32_t)e[0] << 8 | (uint32_t)e[1] << 16 | (uint32_t)e[2] << 24;
-  r.tbl_hi = (uint32_t)e[3] | (uint32_t)e[4] << 8 | (uint32_t)e[5] << 16 | (uint32_t)e[6] << 24;
-  return r;
-}
-
 struct StaticBits {
   uint4 s;                 // 16 sign-mantissa bytes
   uint32_t p0, p1, p2;     // 16 plane bits each
@@ -405,6 +359,13 @@ __device__ __forceinline__ void expand_escapes(const uint8_t* eb, uint32_t esc, 
   }
 }
 
+// kPull: segments are peer frames that become readable at different times
+// (the peer-memory collectives).  Headers are validated lazily,
+// when a CTA first touches a segment after its ready flag reached the epoch,
+// and work is claimed per segment (one counter each, counter[1 + s]) from
+// whichever segment is ready, starting at blockIdx % nseg: decoding of an
+// early peer's frame never waits for a late one.
+template <bool kPull>
 __global__ void __launch_bounds__(kDThreads, ZC_DMINB)   // CTAs / SM (register cap)
 decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restrict__ out,
                    int32_t* __restrict__ err, unsigned* __restrict__ counter, int write_out) {
@@ -437,8 +398,11 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
     }
     s_xsel[m] = sel;
   }
-  if (tid < segs.nseg) {   // every segment's header, validated once per CTA
-    const HeaderInfo h = check_header(segs.stat[tid], segs.n[tid], segs.dyn_len[tid]);
+  if (!kPull && tid < segs.nseg) {   // every segment's header, validated once per CTA
+    HeaderInfo h = check_header(segs.stat[tid], segs.n[tid], segs.dyn_len[tid]);
+    // groups must fit one tile here (gi slices, per-tile escape bounds);
+    // larger groups are the look-back decoder's (flags bit 1)
+    if (h.err == kOk && h.gsl > 12) h.err = kErrGroupTooLarge;
     s_hdr[tid] = h;
     if (h.err != kOk && blockIdx.x == 0) atomicMin(err + tid, h.err);
   }
@@ -457,13 +421,73 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
     const int lane = tid;
     int64_t k = 0;                                   // stages issued
     unsigned cl = 0;
-    if (lane == 0) cl = atomicAdd(counter, 1u);
+    // pull mode bookkeeping (lane 0): segments exhausted / header-checked
+    unsigned long long seg_done = 0, seg_checked = 0;
+    const unsigned long long all_segs =
+        segs.nseg >= 64 ? ~0ull : ((1ull << segs.nseg) - 1ull);
+    int cur = segs.nseg ? (int)(blockIdx.x % (unsigned)segs.nseg) : 0;
+    const uint64_t t_begin = kPull ? globaltimer_ns() : 0;
+    if (!kPull && lane == 0) cl = atomicAdd(counter, 1u);
     int64_t c = (int64_t)__shfl_sync(0xffffffffu, cl, 0);
-    while (c < nchunks) {
+    while (true) {
       unsigned nx = 0;
-      if (lane == 0) nx = atomicAdd(counter, 1u);    // next claim overlaps this chunk
       int seg = 0;
-      while (seg + 1 < segs.nseg && c >= cp.chunk_start[seg + 1]) ++seg;
+      if constexpr (kPull) {
+        int sel = -1, stop = 0;
+        unsigned sel_c = 0;
+        if (lane == 0) {
+          for (int i = 0; i < segs.nseg && sel < 0; ++i) {
+            const int s2 = (cur + i) % segs.nseg;
+            if ((seg_done >> s2) & 1ull) continue;
+            if (!((seg_checked >> s2) & 1ull)) {
+              if (segs.ready[s2] && ld_acquire_sys_u64(segs.ready[s2]) < segs.epoch) continue;
+              // the peer's frame is complete: order the async-proxy (TMA)
+              // reads below after the acquire
+              asm volatile("fence.proxy.async;" ::: "memory");
+              HeaderInfo h = check_header(segs.stat[s2], segs.n[s2], segs.dyn_len[s2]);
+              if (h.err == kOk && h.gsl > 12) h.err = kErrGroupTooLarge;
+              s_hdr[s2] = h;
+              seg_checked |= 1ull << s2;
+              if (h.err != kOk) {
+                atomicMin(err + s2, h.err);
+                seg_done |= 1ull << s2;
+                continue;
+              }
+            }
+            const unsigned cc = atomicAdd(counter + 1 + s2, 1u);
+            if ((int64_t)cc >= cp.chunk_start[s2 + 1] - cp.chunk_start[s2]) {
+              seg_done |= 1ull << s2;
+              continue;
+            }
+            sel = s2;
+            sel_c = cc;
+            cur = s2;
+          }
+          if (sel < 0) {
+            if (seg_done == all_segs) {
+              stop = 1;
+            } else if (segs.timeout_ns > 0 &&
+                       (int64_t)(globaltimer_ns() - t_begin) > segs.timeout_ns) {
+              for (int s2 = 0; s2 < segs.nseg; ++s2)
+                if (!((seg_done >> s2) & 1ull)) atomicMin(err + s2, (int32_t)kErrTimeout);
+              stop = 1;
+            } else {
+              __nanosleep(128);
+            }
+          }
+        }
+        stop = __shfl_sync(0xffffffffu, stop, 0);
+        if (stop) break;
+        sel = __shfl_sync(0xffffffffu, sel, 0);
+        if (sel < 0) continue;
+        seg = sel;
+        c = cp.chunk_start[seg] + (int64_t)__shfl_sync(0xffffffffu, sel_c, 0);
+        __syncwarp();                                  // s_hdr[seg] written by lane 0
+      } else {
+        if (c >= nchunks) break;
+        if (lane == 0) nx = atomicAdd(counter, 1u);    // next claim overlaps this chunk
+        while (seg + 1 < segs.nseg && c >= cp.chunk_start[seg + 1]) ++seg;
+      }
       const HeaderInfo H = s_hdr[seg];
       if (H.err == kOk) {
         const int64_t n = H.n;
@@ -531,7 +555,7 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
           ++k;
         }
       }
-      c = (int64_t)__shfl_sync(0xffffffffu, nx, 0);
+      if (!kPull) c = (int64_t)__shfl_sync(0xffffffffu, nx, 0);
     }
     if (lane == 0) {                  // end markers: one for each consumer group
       for (int e = 0; e < kDGroups; ++e, ++k) {
@@ -875,7 +899,7 @@ static int grid_cap(const void* fn, int threads, size_t dyn) {
 __global__ void decode_init_kernel(int32_t* __restrict__ err, int nseg, unsigned* __restrict__ counter) {
   const int t = threadIdx.x;
   if (t < nseg) err[t] = 0x7F7F7F7F;                // "no error" (atomicMin target)
-  if (t == 0) *counter = 0u;
+  if (t <= nseg) counter[t] = 0u;                   // global claim + per-segment (pull) counters
 }
 
 cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, void* ws,
@@ -896,8 +920,8 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
     uint64_t* status = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ws) + 128);
     e = cudaMemsetAsync(ws, 0, 128 + 8 * ntiles, st);
     if (e != cudaSuccess) return e;
-    static int cap = 0;
-    if (cap == 0) cap = grid_cap((const void*)decode_lookback_kernel, kThreads, 0);
+    static int caps[kMaxDevices];
+    const int cap = per_device(caps, [] { return grid_cap((const void*)decode_lookback_kernel, kThreads, 0); });
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     prof_mark(kProfDecode, false, st);
     decode_lookback_kernel<<<grid, kThreads, 0, st>>>(segs, out, err, status, counter, write_out);
@@ -905,18 +929,23 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
     return cudaGetLastError();
   }
   const size_t dyn = kDStages * kDStageBytes + 2 * kDStages * sizeof(uint64_t);
-  static int cap2 = 0;
-  if (cap2 == 0) {
-    cudaFuncSetAttribute(decode_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    cap2 = grid_cap((const void*)decode_ring_kernel, kDThreads, dyn);
+  const bool pull = (flags >> 2) & 1;
+  static int caps2[kMaxDevices];
+  const int cap2 = per_device(caps2, [dyn] {
+    cudaFuncSetAttribute(decode_ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaFuncSetAttribute(decode_ring_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    int c = grid_cap((const void*)decode_ring_kernel<false>, kDThreads, dyn);
+    const int cp2 = grid_cap((const void*)decode_ring_kernel<true>, kDThreads, dyn);
+    if (cp2 < c) c = cp2;
     if (const char* e = getenv("ZC_DECODE_CTAS_PER_SM")) {
       int dev = 0, sms = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const int want = sms * atoi(e);
-      if (want > 0 && want < cap2) cap2 = want;
+      if (want > 0 && want < c) c = want;
     }
-  }
+    return c;
+  });
   DChunkPlan cp{};
   // inputs of at most one tile per CTA are spread one tile per CTA (a 1 MiB
   // message: 128 CTAs instead of 32; 26.8 against 30.3 us per codec step)
@@ -929,9 +958,12 @@ cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, v
   const int64_t nchunks = cp.chunk_start[segs.nseg];
   const unsigned grid = (unsigned)(nchunks < cap2 ? nchunks : cap2);
   unsigned* counter = reinterpret_cast<unsigned*>(ws);
-  decode_init_kernel<<<1, kMaxSegments, 0, st>>>(err, segs.nseg, counter);
+  decode_init_kernel<<<1, kMaxSegments + 32, 0, st>>>(err, segs.nseg, counter);
   prof_mark(kProfDecode, false, st);
-  decode_ring_kernel<<<grid, kDThreads, dyn, st>>>(segs, cp, out, err, counter, write_out);
+  if (pull)
+    decode_ring_kernel<true><<<grid, kDThreads, dyn, st>>>(segs, cp, out, err, counter, write_out);
+  else
+    decode_ring_kernel<false><<<grid, kDThreads, dyn, st>>>(segs, cp, out, err, counter, write_out);
   prof_mark(kProfDecode, true, st);
   return cudaGetLastError();
 }
@@ -1020,6 +1052,21 @@ cudaError_t launch_decode_groups(const uint8_t* frame, int64_t n, int gsl, int64
   const int64_t ng = g1 - g0;
   const unsigned grid = (unsigned)(ng < 4096 ? ng : 4096);
   decode_groups_kernel<<<grid, kThreads, 0, st>>>(frame, n, gsl, g0, g1, out);
+  return cudaGetLastError();
+}
+
+
+// Loads every kernel of this file now (cudaFuncGetAttributes forces a
+// lazily loaded module function in): with CUDA_MODULE_LOADING=LAZY, the
+// first launch of a kernel waits for the device, which deadlocks while a
+// peer rank sharing the GPU spins on a flag this rank has yet to publish.
+cudaError_t preload_decode() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, (const void*)decode_groups_kernel);
+  cudaFuncGetAttributes(&a, (const void*)decode_init_kernel);
+  cudaFuncGetAttributes(&a, (const void*)decode_lookback_kernel);
+  cudaFuncGetAttributes(&a, (const void*)decode_ring_kernel<false>);
+  cudaFuncGetAttributes(&a, (const void*)decode_ring_kernel<true>);
   return cudaGetLastError();
 }
 

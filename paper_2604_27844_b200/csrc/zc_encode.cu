@@ -850,18 +850,18 @@ static RunPlan make_plan(const EncodeSegs& segs, int cap1) {
 static size_t tiles_dyn_smem() { return kStages * kStageBytes + kStages * sizeof(uint64_t); }
 
 static int tiles_cap() {
-  static int cap1 = 0;
-  if (cap1 == 0) {
+  static int caps[kMaxDevices];
+  return per_device(caps, [] {
     cudaFuncSetAttribute(encode_tiles_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tiles_dyn_smem());
     cudaFuncSetAttribute(encode_tiles_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tiles_dyn_smem());
-    cap1 = grid_for((const void*)encode_tiles_kernel<false>, kThreads, tiles_dyn_smem());
+    int cap1 = grid_for((const void*)encode_tiles_kernel<false>, kThreads, tiles_dyn_smem());
     const int cap2 = grid_for((const void*)encode_tiles_kernel<true>, kThreads, tiles_dyn_smem());
     if (cap2 < cap1) cap1 = cap2;   // one plan serves both (the re-encode reuses it)
     if (cap1 > 4096) cap1 = 4096;
-  }
-  return cap1;
+    return cap1;
+  });
 }
 
 // pass 1 + run fix-up; optional fused certificate (spec) / conditional
@@ -906,8 +906,8 @@ cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8
       cudaError_t e = cudaMemsetAsync(ws, 0, kLbStatusOff + 8 * ntiles, st);
       if (e != cudaSuccess) return e;
     }
-    static int cap = 0;
-    if (cap == 0) cap = grid_for((const void*)encode_lookback_kernel, kThreads, 0);
+    static int caps[kMaxDevices];
+    const int cap = per_device(caps, [] { return grid_for((const void*)encode_lookback_kernel, kThreads, 0); });
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     encode_lookback_kernel<<<grid, kThreads, 0, st>>>(x, segs, book, frames, status, counter,
                                                        frame_len);
@@ -985,6 +985,21 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms, st);
   if (e != cudaSuccess) return e;
   return launch_two_pass(x, segs, rp2, book, frames, w8, frame_len, nullptr, guess, st);
+}
+
+
+// Loads every kernel of this file now (cudaFuncGetAttributes forces a
+// lazily loaded module function in): with CUDA_MODULE_LOADING=LAZY, the
+// first launch of a kernel waits for the device, which deadlocks while a
+// peer rank sharing the GPU spins on a flag this rank has yet to publish.
+cudaError_t preload_encode() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, (const void*)encode_lookback_kernel);
+  cudaFuncGetAttributes(&a, (const void*)encode_runfix_kernel);
+  cudaFuncGetAttributes(&a, (const void*)encode_tiles_kernel<false>);
+  cudaFuncGetAttributes(&a, (const void*)encode_tiles_kernel<true>);
+  tiles_cap();
+  return cudaGetLastError();
 }
 
 }  // namespace zc

@@ -133,17 +133,16 @@ stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs,
 static size_t stats_dyn_smem() { return kSStages * kSStageBytes + kSStages * sizeof(uint64_t); }
 
 static int stats_grid_cap() {
-  static int cap = 0;
-  if (cap == 0) {
+  static int caps[kMaxDevices];
+  return per_device(caps, [] {
     cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)stats_dyn_smem());
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stats_kernel, kThreads, stats_dyn_smem());
-    cap = sms * (occ > 0 ? occ : 1);
-  }
-  return cap;
+    return sms * (occ > 0 ? occ : 1);
+  });
 }
 
 // Fixed-order merge of `nparts` partials by one kThreads-thread CTA (each
@@ -310,15 +309,14 @@ sums_kernel(const uint16_t* __restrict__ x, const StatSegs segs, SumPartial* __r
 }
 
 static int sums_grid_cap() {
-  static int cap = 0;
-  if (cap == 0) {
+  static int caps[kMaxDevices];
+  return per_device(caps, [] {
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sums_kernel, kThreads, 0);
-    cap = sms * (occ > 0 ? occ : 1);
-  }
-  return cap;
+    return sms * (occ > 0 ? occ : 1);
+  });
 }
 
 
@@ -514,6 +512,24 @@ cudaError_t launch_exact_if_needed(const uint16_t* x, const StatSegs& segs, int6
   if (grid > ntiles) grid = ntiles;
   stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(
       x, segs, parts, done, total, book, result, need);
+  return cudaGetLastError();
+}
+
+
+// Loads every kernel of this file now (cudaFuncGetAttributes forces a
+// lazily loaded module function in): with CUDA_MODULE_LOADING=LAZY, the
+// first launch of a kernel waits for the device, which deadlocks while a
+// peer rank sharing the GPU spins on a flag this rank has yet to publish.
+cudaError_t preload_stats() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, (const void*)finalize_kernel);
+  cudaFuncGetAttributes(&a, (const void*)guess_kernel);
+  cudaFuncGetAttributes(&a, (const void*)hist_kernel);
+  cudaFuncGetAttributes(&a, (const void*)mode_kernel);
+  cudaFuncGetAttributes(&a, (const void*)stats_kernel);
+  cudaFuncGetAttributes(&a, (const void*)sums_kernel);
+  stats_grid_cap();
+  sums_grid_cap();
   return cudaGetLastError();
 }
 

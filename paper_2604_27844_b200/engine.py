@@ -267,6 +267,7 @@ ERR_FIELDS = {
     18: ("zero_count", "planes disagree with zero_exponents"),
     19: ("element_count", "frame holds a different element count than expected"),
     20: ("timeout", "peer frame never became ready"),
+    21: ("group_size_log2", "groups larger than 4096 elements need the large-group decoder"),
 }
 
 

@@ -45,14 +45,33 @@ class TrafficStats:
 
 
 class Communicator:
-    """A rank bound into a group of ``world_size`` peers (transport.py:576-623)."""
+    """A rank bound into a group of ``world_size`` peers (transport.py:576-623).
+
+    ``native`` (when set) is the rank's NativeComm: the collectives then run
+    the C++ engine (native.py); ``use_native = False`` forces the generic
+    Python protocols over this communicator's byte movers."""
 
     rank: int
     world_size: int
     device: torch.device
+    native = None
+    use_native = True
 
     def __init__(self):
-        self.stats = TrafficStats()
+        self._stats = TrafficStats()
+
+    @property
+    def stats(self) -> TrafficStats:
+        """Bytes this rank put on the wire: the generic protocols' counters
+        plus the native engine's (host-side message plane, device-side
+        peer-memory plane; reading them synchronises the device)."""
+        s = self._stats.snapshot()
+        nat = self.__dict__.get("native") or self.__dict__.get("_native")
+        if nat is not None:
+            b, m = nat.stats()
+            s.bytes_sent += b
+            s.messages_sent += m
+        return s
 
     # -- reference surface -------------------------------------------------------
     def peers(self) -> list:
@@ -75,13 +94,23 @@ class Communicator:
     def allgather_ints(self, value: int) -> list:
         return self._allgather_ints(int(value))
 
+    def allgather_vec(self, values) -> list:
+        """All-gather a short int vector per rank; row p is rank p's."""
+        return self._allgather_vec([int(v) for v in values])
+
     # -- byte movers (device tensors) ------------------------------------------
     def all_gather_bytes(self, send: torch.Tensor, recv: torch.Tensor) -> None:
         """recv[p*len(send):(p+1)*len(send)] = send of rank p (equal sizes)."""
         raise NotImplementedError
 
-    def sendrecv_bytes(self, sends: dict, recvs: dict) -> None:
-        """Grouped point-to-point: sends {peer: tensor}, recvs {peer: tensor}."""
+    def sendrecv_bytes(self, sends: dict, recvs: dict, label: str = "message") -> None:
+        """Grouped point-to-point: sends {peer: tensor}, recvs {peer: tensor}.
+
+        Receive sizes are the receiver's expectation (the reference's
+        pre-sized receives, collectives.py:294-305).  Transports that can see
+        both sides (the thread hub) raise ProtocolError naming ``label`` on a
+        size disagreement; NCCL cannot, so callers that need the check agree
+        on sizes first (``comm.check_counts``)."""
         raise NotImplementedError
 
     def barrier(self) -> None:
@@ -89,8 +118,8 @@ class Communicator:
 
     # -- helpers -----------------------------------------------------------------
     def _count(self, nbytes: int, nmsg: int = 1) -> None:
-        self.stats.bytes_sent += int(nbytes)
-        self.stats.messages_sent += int(nmsg)
+        self._stats.bytes_sent += int(nbytes)
+        self._stats.messages_sent += int(nmsg)
 
     @classmethod
     def from_process_group(cls, group=None, device=None) -> "DistCommunicator":
@@ -113,6 +142,18 @@ class DistCommunicator(Communicator):
                 if torch.cuda.is_available() else torch.device("cpu")
         self.device = torch.device(device)
         self.on_device = self.backend == "nccl"
+        self._native = None
+
+    @property
+    def native(self):
+        """Native engine over this NCCL group, created (collectively) by the
+        first collective that needs it; None on gloo (the generic path)."""
+        if not self.on_device or not self.use_native:
+            return None
+        if self._native is None:
+            from .native import NativeComm
+            self._native = NativeComm.from_process_group(self.group, self.device)
+        return self._native
 
     def _wire(self, t: torch.Tensor) -> torch.Tensor:
         return t if self.on_device else t.cpu()
@@ -123,6 +164,15 @@ class DistCommunicator(Communicator):
         out = torch.empty(self.world_size, dtype=torch.int64, device=dev)
         self._dist.all_gather_into_tensor(out, src, group=self.group)
         return [int(v) for v in out.cpu().tolist()]
+
+    def _allgather_vec(self, values: list) -> list:
+        dev = self.device if self.on_device else torch.device("cpu")
+        src = torch.tensor(values, dtype=torch.int64, device=dev)
+        out = torch.empty(self.world_size * len(values), dtype=torch.int64, device=dev)
+        self._dist.all_gather_into_tensor(out, src, group=self.group)
+        flat = [int(v) for v in out.cpu().tolist()]
+        k = len(values)
+        return [flat[p * k:(p + 1) * k] for p in range(self.world_size)]
 
     def _a2a_ints(self, sizes: list) -> list:
         dev = self.device if self.on_device else torch.device("cpu")
@@ -141,7 +191,7 @@ class DistCommunicator(Communicator):
         self._count(send.numel() * send.element_size() * (self.world_size - 1),
                     self.world_size - 1)
 
-    def sendrecv_bytes(self, sends: dict, recvs: dict) -> None:
+    def sendrecv_bytes(self, sends: dict, recvs: dict, label: str = "message") -> None:
         dist = self._dist
         staged = {}
         ops = []
@@ -207,19 +257,23 @@ class _Hub:
 class HubCommunicator(Communicator):
     """Thread rank on a shared hub; each rank has its own CUDA stream."""
 
-    def __init__(self, hub: _Hub, rank: int, device):
+    def __init__(self, hub: _Hub, rank: int, device, native=None):
         super().__init__()
         self.hub = hub
         self.rank = rank
         self.world_size = hub.world_size
         self.device = torch.device(device)
         self.stream = torch.cuda.Stream(device=self.device)
+        self.native = native
 
     def _post_and_collect(self, obj) -> list:
         return self.hub.exchange(self.rank, obj)
 
     def _allgather_ints(self, value: int) -> list:
         return [int(v) for v in self._post_and_collect(int(value))]
+
+    def _allgather_vec(self, values: list) -> list:
+        return [list(r) for r in self._post_and_collect(list(values))]
 
     def _a2a_ints(self, sizes: list) -> list:
         rows = self._post_and_collect(list(sizes))
@@ -237,16 +291,22 @@ class HubCommunicator(Communicator):
         self.hub.sync(self.rank)
         self._count(n * send.element_size() * (self.world_size - 1), self.world_size - 1)
 
-    def sendrecv_bytes(self, sends: dict, recvs: dict) -> None:
+    def sendrecv_bytes(self, sends: dict, recvs: dict, label: str = "message") -> None:
         torch.cuda.current_stream(self.device).synchronize()
-        posted = self._post_and_collect({p: t for p, t in sends.items()})
-        for p, t in recvs.items():
-            if t.numel():
-                src = posted[p].get(self.rank)
-                if src is None or src.numel() != t.numel():
-                    got = 0 if src is None else src.numel()
-                    raise ProtocolError(f"rank {p} sent {got} bytes, expected {t.numel()}")
+        posted = self._post_and_collect({p: t for p, t in sends.items() if t.numel()})
+        bad = None
+        for p in self.peers():
+            src = posted[p].get(self.rank)
+            got = 0 if src is None else src.numel()
+            t = recvs.get(p)
+            want = 0 if t is None else t.numel()
+            if got != want:
+                bad = bad or (p, got, want)
+            elif want:
                 t.copy_(src)
+        if bad is not None:
+            p, got, want = bad
+            raise ProtocolError(f"{label} from rank {p} is {got} bytes, expected {want}")
         torch.cuda.current_stream(self.device).synchronize()
         self.hub.sync(self.rank)
         for t in sends.values():
@@ -258,20 +318,32 @@ class HubCommunicator(Communicator):
         self.hub.sync(self.rank)
 
 
-def run_ranks(world_size: int, fn, device=None, timeout: float = DEFAULT_TIMEOUT) -> list:
+def run_ranks(world_size: int, fn, device=None, timeout: float = DEFAULT_TIMEOUT,
+              native: bool | None = None) -> list:
     """Run fn(comm) on ``world_size`` in-process thread ranks sharing one GPU
     (or ``device`` per rank when a list is given); results by rank
     (reference run_ranks, transport.py:635-666).  The first failure aborts
-    the hub so peers error out instead of hanging, and is re-raised."""
+    the hub so peers error out instead of hanging, and is re-raised.
+
+    ``native`` (default: up to 64 ranks) gives every rank a native
+    communicator of one in-process group, so the collectives run the C++
+    engine exactly as NCCL ranks do; False keeps the generic protocols."""
     hub = _Hub(world_size)
     results = [None] * world_size
     failures = []
     devs = device if isinstance(device, (list, tuple)) else [device] * world_size
+    devs = [d if d is not None else torch.device("cuda", 0) for d in devs]
+    if native is None:
+        native = 1 < world_size <= 64
+    comms = None
+    if native:
+        from .native import NativeComm
+        comms = NativeComm.local_group(world_size, devs)
 
     def body(rank: int) -> None:
-        dev = devs[rank] if devs[rank] is not None else torch.device("cuda", 0)
+        dev = devs[rank]
         torch.cuda.set_device(dev)
-        comm = HubCommunicator(hub, rank, dev)
+        comm = HubCommunicator(hub, rank, dev, comms[rank] if comms else None)
         try:
             with torch.cuda.stream(comm.stream):
                 results[rank] = fn(comm)
@@ -279,12 +351,17 @@ def run_ranks(world_size: int, fn, device=None, timeout: float = DEFAULT_TIMEOUT
         except BaseException as exc:  # noqa: BLE001 - propagated to the caller
             failures.append((rank, exc))
             hub.abort(exc)
+            for c in comms or ():
+                c.abort()
 
     threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world_size)]
     for t in threads:
         t.start()
     for t in threads:
         t.join(timeout=timeout * 10)
+    if comms:
+        for c in comms:
+            c.close()
     if failures:
         rank, exc = min(failures, key=lambda f: f[0])
         raise exc

@@ -19,7 +19,24 @@ from paper_2604_27844_b200.collectives import (  # noqa: E402
     timed_call, zip_all_gather, zip_all_reduce, zip_all_to_all_d1, zip_all_to_all_d2,
     zip_reduce_scatter)
 from paper_2604_27844_b200.errors import CollectiveError, ProtocolError  # noqa: E402
-from paper_2604_27844_b200.transport import run_ranks  # noqa: E402
+from paper_2604_27844_b200.transport import run_ranks as _run_ranks  # noqa: E402
+
+# every protocol runs on three implementations: the native engine's
+# peer-memory plane, its message plane (the reference's protocols over the
+# in-process device-copy transport that stands in for NCCL), and the generic
+# Python protocols over the thread hub
+MODES = ["p2p", "msg", "generic"]
+
+
+def run_ranks(world, body, mode="p2p", **kw):
+    def wrapped(comm):
+        if mode == "generic":
+            comm.use_native = False
+        elif comm.native is not None:
+            comm.native.plane = "msg" if mode.startswith("msg") else "p2p"
+            comm.native.pipeline = mode == "msg_pipe"
+        return body(comm)
+    return _run_ranks(world, wrapped, native=(mode != "generic") and world <= 64, **kw)
 
 
 def H(t):
@@ -33,23 +50,29 @@ def _a2a_spec(comm, sizer, seed=0):
     return AlltoAllSpec(chunks, counts)
 
 
+@pytest.mark.parametrize("mode", MODES + ["msg_pipe"])
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
-def test_all_gather_matches_reference(world):
+def test_all_gather_matches_reference(world, mode):
     def body(comm):
-        local = rank_words(comm.rank, 4096 * 5 + 17)
-        return H(zip_all_gather(comm, local)), H(reference_all_gather(comm, local))
-    for z, r in run_ranks(world, body):
-        assert np.array_equal(z, r)
+        outs = []
+        for it in range(3):   # epochs: slot reuse guarded by the done flags
+            local = rank_words(comm.rank + 7 * it, 4096 * 5 + 17 + it)
+            outs.append((H(zip_all_gather(comm, local)), H(reference_all_gather(comm, local))))
+        return outs
+    for outs in run_ranks(world, body, mode):
+        for z, r in outs:
+            assert np.array_equal(z, r)
 
 
-def test_all_gather_large_and_specials():
+@pytest.mark.parametrize("mode", MODES)
+def test_all_gather_large_and_specials(mode):
     def body(comm):
         local = rank_words(comm.rank, 3_000_001, sigma=0.02)
         local[:8] = [0x7FC0, 0x7F80, 0xFF80, 0, 0x8000, 1, 0x7F81, 0xFFFF]
         z = zip_all_gather(comm, local)
         return H(z), np.concatenate([rank_words(r, 3_000_001, sigma=0.02)
                                      for r in range(comm.world_size)])
-    outs = run_ranks(3, body)
+    outs = run_ranks(3, body, mode)
     for z, expect in outs:
         expect = expect.copy()
         for r in range(3):
@@ -67,17 +90,22 @@ def test_all_gather_all_nan_payloads():
         assert np.array_equal(z, r)
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("fn", [zip_all_to_all_d1, zip_all_to_all_d2])
 @pytest.mark.parametrize("sizer", [lambda s, d: 2000, lambda s, d: s * 1024 + 64,
                                    lambda s, d: 0 if d == 1 else 300,
-                                   lambda s, d: (s + d) * 97 + 5])
-def test_all_to_all_matches_reference(fn, sizer):
+                                   lambda s, d: (s + d) * 97 + 5],
+                         ids=["equal", "ramp", "skip1", "mixed"])
+def test_all_to_all_matches_reference(fn, sizer, mode):
     def body(comm):
-        spec = _a2a_spec(comm, sizer)
-        z = fn(comm, spec)
-        r = reference_all_to_all(comm, spec)
-        return all(np.array_equal(H(a), H(b)) for a, b in zip(z, r))
-    assert all(run_ranks(3 if sizer(0, 1) == 0 else 4, body))
+        ok = True
+        for it in range(2):
+            spec = _a2a_spec(comm, sizer, seed=it)
+            z = fn(comm, spec)
+            r = reference_all_to_all(comm, spec)
+            ok &= all(np.array_equal(H(a), H(b)) for a, b in zip(z, r))
+        return ok
+    assert all(run_ranks(3 if sizer(0, 1) == 0 else 4, body, mode))
 
 
 def test_all_to_all_moe_dispatch_shape():
@@ -92,28 +120,30 @@ def test_all_to_all_moe_dispatch_shape():
     assert all(run_ranks(4, body))
 
 
-def test_protocol_errors():
+@pytest.mark.parametrize("mode", MODES)
+def test_protocol_errors(mode):
     def d1(comm):
         chunks = [rank_words(q, 100) for q in range(2)]
         expected = 100 if comm.rank == 1 else 50
         return zip_all_to_all_d1(comm, AlltoAllSpec(chunks, [expected] * 2))
     with pytest.raises(ProtocolError, match="expected 50"):
-        run_ranks(2, d1)
+        run_ranks(2, d1, mode)
 
     def d2(comm):
         n = 128 if comm.rank == 0 else 256
         chunks = [rank_words(q, n) for q in range(2)]
         return zip_all_to_all_d2(comm, AlltoAllSpec(chunks, [n] * 2))
     with pytest.raises(ProtocolError, match="static section"):
-        run_ranks(2, d2)
+        run_ranks(2, d2, mode)
 
     def ag(comm):
         return zip_all_gather(comm, rank_words(comm.rank, 10 + comm.rank))
     with pytest.raises(CollectiveError, match="peer rank"):
-        run_ranks(2, ag)
+        run_ranks(2, ag, mode)
 
 
-def test_zero_element_collectives():
+@pytest.mark.parametrize("mode", MODES)
+def test_zero_element_collectives(mode):
     def body(comm):
         empty = np.empty(0, dtype=np.uint16)
         ag = zip_all_gather(comm, empty)
@@ -123,16 +153,17 @@ def test_zero_element_collectives():
                                                    [0] * comm.world_size))
         rs = zip_reduce_scatter(comm, empty)
         return ag.numel() == 0 and all(c.numel() == 0 for c in a2a + a2b) and rs.numel() == 0
-    assert all(run_ranks(3, body))
+    assert all(run_ranks(3, body, mode))
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_reduce_scatter_matches_reference_and_oracle(world):
+def test_reduce_scatter_matches_reference_and_oracle(world, mode):
     def body(comm):
         local = rank_words(comm.rank, comm.world_size * 1000)
         return (H(zip_reduce_scatter(comm, local)), H(reference_reduce_scatter(comm, local)),
                 zip_reduce_scatter(comm, local, output="fp32").cpu().numpy())
-    outs = run_ranks(world, body)
+    outs = run_ranks(world, body, mode)
     shard = 1000
     for r, (z, ref, f32) in enumerate(outs):
         assert np.array_equal(z, ref)
@@ -143,7 +174,8 @@ def test_reduce_scatter_matches_reference_and_oracle(world):
         assert np.array_equal(z, zo.from_f32(acc))
 
 
-def test_fp32_accumulation_contract():
+@pytest.mark.parametrize("mode", MODES)
+def test_fp32_accumulation_contract(mode):
     # reference tests/test_collectives.py:215-241
     def body(comm):
         value = 1.0 if comm.rank == 0 else 2.0 ** -8
@@ -153,34 +185,64 @@ def test_fp32_accumulation_contract():
     for _ in range(3):
         expected32 = np.float32(expected32 + np.float32(2.0 ** -8))
     word = int(zo.from_f32(np.array([expected32], np.float32))[0])
-    for out in run_ranks(4, body):
+    for out in run_ranks(4, body, mode):
         assert np.all(out == word)
 
 
-def test_all_reduce_composition():
+@pytest.mark.parametrize("mode", MODES)
+def test_all_reduce_composition(mode):
     def body(comm):
         local = rank_words(comm.rank, 4 * 64)
         got = zip_all_reduce(comm, local)
         expect = reference_all_gather(comm, reference_reduce_scatter(comm, local))
         return np.array_equal(H(got), H(expect))
-    assert all(run_ranks(4, body))
+    assert all(run_ranks(4, body, mode))
 
 
-def test_traffic_is_compressed():
+@pytest.mark.parametrize("mode", ["msg", "generic"])
+def test_wire_bytes_match_size_law(mode):
+    # reference tests/test_collectives.py:274-302: design 1 sends the frames
+    # plus 16 B of metadata per peer; design 2 the same frames plus 8 B
     n_chunk = 1 << 16
+    world = 4
+
+    def body(comm):
+        spec = _a2a_spec(comm, lambda s, d: n_chunk, seed=12)
+        before = comm.stats.snapshot()
+        zip_all_to_all_d1(comm, spec)
+        d1 = comm.stats.snapshot().delta(before).bytes_sent
+        before = comm.stats.snapshot()
+        zip_all_to_all_d2(comm, spec)
+        d2 = comm.stats.snapshot().delta(before).bytes_sent
+        frames = zo.peer_frames(list(spec.send_chunks), comm.rank)
+        return d1, d2, sum(len(f) for f in frames)
+    for d1, d2, frames in run_ranks(world, body, mode):
+        assert d1 == frames + 16 * (world - 1)
+        assert d2 == frames + 8 * (world - 1)
+        assert d1 - d2 == 3 * 8                       # reference test_collectives.py:304-317
+        assert 2 * n_chunk * (world - 1) / d2 >= 1.30
+
+
+def test_p2p_traffic_accounting():
+    # peer-memory plane: each peer pulls its frame once; ready + done flags
+    # are 8 B per peer each
+    n_chunk = 1 << 16
+    world = 4
 
     def body(comm):
         spec = _a2a_spec(comm, lambda s, d: n_chunk, seed=12)
         before = comm.stats.snapshot()
         zip_all_to_all_d2(comm, spec)
         sent = comm.stats.snapshot().delta(before).bytes_sent
-        sendable = [spec.send_chunks[q] for q in range(comm.world_size) if q != comm.rank]
         frames = zo.peer_frames(list(spec.send_chunks), comm.rank)
-        return sent, sum(len(f) for f in frames)
-    world = 4
-    for sent, frames in run_ranks(world, body):
-        assert sent == frames + 16 * (world - 1)   # frames + counts + dynamic sizes
-        assert 2 * n_chunk * (world - 1) / sent >= 1.30
+        ag_before = comm.stats.snapshot()
+        local = rank_words(comm.rank, n_chunk)
+        zip_all_gather(comm, local)
+        ag = comm.stats.snapshot().delta(ag_before).bytes_sent
+        return sent, sum(len(f) for f in frames), ag, len(zo.encode(local, zo.book_for(local)))
+    for sent, frames, ag, f in run_ranks(world, body, "p2p"):
+        assert sent == frames + 16 * (world - 1)
+        assert ag == (f + 16) * (world - 1)
 
 
 def test_timed_call_agrees():
@@ -191,7 +253,8 @@ def test_timed_call_agrees():
     assert len(set(ts)) == 1 and ts[0] > 0
 
 
-def test_fuzz_against_reference():
+@pytest.mark.parametrize("mode", MODES)
+def test_fuzz_against_reference(mode):
     # reference tests/test_acceptance.py:155-207 on the GPU path
     for world in (2, 3, 4):
         for seed in (0, 1):
@@ -221,35 +284,4 @@ def test_fuzz_against_reference():
                     if not all(np.array_equal(H(a), H(b)) for a, b in zip(got, ref)):
                         return False
                 return True
-            assert all(run_ranks(world, body)), (world, seed)
-
-
-@pytest.mark.parametrize("world", [2, 3, 4])
-def test_all_gather_p2p_pull_decode(world):
-    from paper_2604_27844_b200.collectives import zip_all_gather_p2p
-
-    def body(comm):
-        outs = []
-        for it in range(3):   # epochs: buffer reuse is guarded by the done flags
-            local = rank_words(comm.rank + 10 * it, 300_007, sigma=0.02)
-            outs.append((H(zip_all_gather_p2p(comm, local)), H(reference_all_gather(comm, local))))
-        return outs
-    for outs in run_ranks(world, body):
-        for z, r in outs:
-            assert np.array_equal(z, r)
-
-
-@pytest.mark.parametrize("sizer", [lambda s, d: 4096 * 3 + 17, lambda s, d: (s + d) * 97 + 5,
-                                   lambda s, d: 0 if d == 1 else 5000 + s])
-def test_all_to_all_p2p_pull_decode(sizer):
-    from paper_2604_27844_b200.collectives import zip_all_to_all_p2p
-
-    def body(comm):
-        ok = True
-        for it in range(3):
-            spec = _a2a_spec(comm, sizer, seed=it)
-            z = zip_all_to_all_p2p(comm, spec)
-            r = reference_all_to_all(comm, spec)
-            ok &= all(np.array_equal(H(a), H(b)) for a, b in zip(z, r))
-        return ok
-    assert all(run_ranks(4, body))
+            assert all(run_ranks(world, body, mode)), (world, seed)
