@@ -76,6 +76,7 @@ EXPORTS = {
     "zc_reduce_frames": (_int, [_vp, _int, _i64, _vp, _int, _vp, _vp, _vp]),
     "zc_reduce_scratch_bytes": (_i64, [_int]),
     "zc_red_src_bytes": (_int, []),
+    "zc_estimate_ratio": (_int, [_vp, _i64, _vp, _vp, _vp]),
 }
 
 

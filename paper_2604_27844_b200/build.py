@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libzipccl_b200.so"
 SOURCES = ["zc_abi.cu", "zc_encode.cu", "zc_decode.cu", "zc_stats.cu", "zc_p2p.cu",
-           "zc_reduce.cu", "zc_coll.cu"]
+           "zc_reduce.cu", "zc_coll.cu", "zc_estimate.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

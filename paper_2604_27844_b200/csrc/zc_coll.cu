@@ -58,6 +58,7 @@ cudaError_t preload_encode();
 cudaError_t preload_decode();
 cudaError_t preload_stats();
 cudaError_t preload_reduce();
+cudaError_t preload_estimate();
 }  // namespace zc
 
 extern "C" int64_t zc_workspace_bytes(int64_t total_elems, int nseg);
@@ -1186,6 +1187,7 @@ static int comm_common_init(zc_comm* c, int64_t slot_bytes) {
   preload_decode();
   preload_stats();
   preload_reduce();
+  preload_estimate();
   {
     cudaFuncAttributes a;
     const void* ks[] = {(const void*)publish_kernel, (const void*)wait_flags_kernel,

@@ -86,6 +86,21 @@ def book_tensor(entries, device) -> torch.Tensor:
     return _book_cached(tuple(int(e) for e in entries), device.index or 0)
 
 
+def _merge_segments(segs) -> list:
+    """Adjacent segments as one range (the statistic only sees their union):
+    the non-self chunks of a packed all-to-all buffer are at most two ranges,
+    however many peers there are."""
+    out = []
+    for o, n in segs:
+        if n <= 0:
+            continue
+        if out and out[-1][0] + out[-1][1] == o:
+            out[-1] = (out[-1][0], out[-1][1] + n)
+        else:
+            out.append((o, n))
+    return out or [(0, 0)]
+
+
 SIGMA_EXACT = 1   # zc_codebook_measured flag (include/zipccl_b200.h)
 MAX_SEGMENTS_MEASURED = _lib.MAX_SEGMENTS   # segments per zc_encode_measured call
 
@@ -99,6 +114,7 @@ def measured_codebook(words: torch.Tensor, segs=None, stream=None, exact: bool =
     """
     if segs is None:
         segs = [(0, words.numel())]
+    segs = _merge_segments(segs)
     dev = words.device
     book = torch.empty(8, dtype=torch.uint8, device=dev)
     result = torch.empty(3, dtype=torch.float64, device=dev)
@@ -116,6 +132,7 @@ def modal_codebook(words: torch.Tensor, segs=None, stream=None) -> torch.Tensor:
     """Histogram-mode codebook (reference codec.py:181-185) for explicit bad sigma."""
     if segs is None:
         segs = [(0, words.numel())]
+    segs = _merge_segments(segs)
     dev = words.device
     book = torch.empty(8, dtype=torch.uint8, device=dev)
     total = sum(n for _, n in segs)
@@ -224,6 +241,21 @@ def decode_groups(frame: torch.Tensor, n: int, gs_log2: int, g0: int, g1: int,
     if count:
         check(lib().zc_decode_groups(frame.data_ptr(), int(n), int(gs_log2), int(g0), int(g1),
                                      out.data_ptr(), stream_ptr(stream)), "zc_decode_groups")
+    return out
+
+
+def estimate_ratio(words: torch.Tensor, stream=None) -> torch.Tensor:
+    """Estimated compression factor (frame / raw bytes) of ``words`` under the
+    codebook codebook_for would pick, from a 1/64 sample (zc_estimate_ratio):
+    float64[3] device tensor (e, sample sigma, sample escape fraction)."""
+    out = torch.empty(3, dtype=torch.float64, device=words.device)
+    n = words.numel()
+    if n == 0:
+        out.fill_(1.0)
+        return out
+    with workspace(n, 1, words.device, stream) as ws:
+        check(lib().zc_estimate_ratio(words.data_ptr(), n, ws.data_ptr(), out.data_ptr(),
+                                      stream_ptr(stream)), "zc_estimate_ratio")
     return out
 
 

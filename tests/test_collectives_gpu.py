@@ -285,3 +285,51 @@ def test_fuzz_against_reference(mode):
                         return False
                 return True
             assert all(run_ranks(world, body, mode)), (world, seed)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_reduce_scatter_nan_inf_semantics(mode):
+    # numpy's float32 add on x86 (the reference's arithmetic): a NaN operand
+    # propagates quieted, inf + -inf is the default NaN 0xFFC00000; the RNE
+    # narrowing keeps sign and top payload bits and forces the quiet bit
+    # (bf16.py:53-66).  One NaN per element at most (NaN + NaN payload choice
+    # is position-dependent in numpy itself).
+    specials = {0: 0x7F81, 1: 0xFFA5, 2: 0x7F80, 3: 0xFF80, 4: 0x0001, 5: 0x8001,
+                6: 0x7F7F, 7: 0xFF7F}
+
+    def body(comm):
+        W = comm.world_size
+        local = rank_words(comm.rank, W * 1024, seed=9)
+        for j, w in specials.items():
+            if j % W == comm.rank:        # element j of every shard gets a special
+                for r in range(W):
+                    local[r * 1024 + j] = w
+        if comm.rank == 1:
+            for r in range(W):
+                local[r * 1024 + 20] = 0x7F80   # +inf from rank 1 ...
+        if comm.rank == 2:
+            for r in range(W):
+                local[r * 1024 + 20] = 0xFF80   # ... -inf from rank 2
+        return (H(zip_reduce_scatter(comm, local)), H(reference_reduce_scatter(comm, local)),
+                zip_reduce_scatter(comm, local, output="fp32").cpu().numpy(), local)
+    outs = run_ranks(4, body, mode)
+    locals_ = [o[3] for o in outs]
+    for r, (z, ref, f32, _) in enumerate(outs):
+        acc = zo.to_f32(locals_[0][r * 1024:(r + 1) * 1024]).copy()
+        with np.errstate(invalid="ignore", over="ignore"):
+            for p in range(1, 4):
+                acc += zo.to_f32(locals_[p][r * 1024:(r + 1) * 1024])
+        assert np.array_equal(f32.view(np.uint32), acc.view(np.uint32))
+        assert np.array_equal(z, zo.from_f32(acc)) and np.array_equal(z, ref)
+        assert f32.view(np.uint32)[20] == 0xFFC00000
+
+
+def test_reduce_scatter_257_ranks_fp32_contract():
+    # reference tests/test_acceptance.py:222-248 (criterion 6): 257 ranks,
+    # shard of 1 element; generic protocols (more ranks than a native group)
+    def body(comm):
+        value = 1.0 if comm.rank == 0 else 2.0 ** -8
+        local = zo.from_f64(np.full(comm.world_size, value))
+        return H(zip_reduce_scatter(comm, local))
+    outs = run_ranks(257, body, "generic", timeout=300.0)
+    assert all(o.size == 1 and int(o[0]) == 0x4000 for o in outs)
