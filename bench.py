@@ -139,22 +139,79 @@ def _agreed_steps(seconds, step, world, dev):
     return int(k.item())
 
 
-def _preflight_p2p(comm, coll, dev) -> bool:
-    """Run one small pull-decode all-gather and check it against the plain
-    collective; any failure on any rank falls back to the NCCL data plane."""
+def setup_comm(args, dev):
+    """Communicator for N>1: the native engine over the NCCL group (peer-
+    memory plane when every peer's buffer maps, else the message plane),
+    checked against a bare NCCL all-gather on a small message before
+    anything is timed.  Any failure on any rank falls back, identically on
+    all ranks: p2p -> message plane -> generic protocols over NCCL."""
     import torch
     import torch.distributed as dist
-    ok = 1
+    from paper_2604_27844_b200 import collectives as coll
+    comm = coll.Communicator.from_process_group()
+    g = torch.Generator(device=dev).manual_seed(1234 + comm.rank)
+    x = (torch.randn((1 << 20) + 77, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    ref = torch.empty(comm.world_size * x.numel(), dtype=torch.bfloat16, device=dev)
+    dist.all_gather_into_tensor(ref, x)
+    want = "p2p" if args.transport == "p2p" else "msg"
+    tried = []
+    for plane in ([want, "msg", "generic"] if want == "p2p" else [want, "generic"]):
+        ok = 1
+        try:
+            if plane == "generic":
+                comm.use_native = False
+            else:
+                comm.use_native = True
+                native = comm.native
+                if plane == "p2p" and not native.p2p_available:
+                    ok = 0
+                native.plane = plane
+            if ok:
+                got = coll.zip_all_gather(comm, x)
+                ok = int(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
+        except Exception as exc:  # noqa: BLE001 - any failure selects the fallback
+            print(f"[rank {comm.rank}] {plane} preflight failed: {exc!r}", file=sys.stderr)
+            ok = 0
+        t = torch.tensor([ok], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        tried.append(plane)
+        if t.item():
+            comm.bench_plane = plane
+            comm.bench_tried = tried
+            if plane != "generic":
+                comm.native.sync_errors = False       # checked after the timed region
+            return comm
+    raise RuntimeError("no data plane passed the preflight")
+
+
+def nccl_info():
+    import torch
     try:
-        g = torch.Generator(device=dev).manual_seed(1234 + comm.rank)
-        x = (torch.randn(1 << 20, device=dev, generator=g) * 0.02).to(torch.bfloat16)
-        ok = int(torch.equal(coll.zip_all_gather_p2p(comm, x), coll.reference_all_gather(comm, x)))
-    except Exception as exc:  # noqa: BLE001 - any failure selects the fallback
-        print(f"[rank {comm.rank}] p2p preflight failed: {exc!r}", file=sys.stderr)
-        ok = 0
-    t = torch.tensor([ok], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MIN)
-    return bool(t.item())
+        v = torch.cuda.nccl.version()
+        ver = ".".join(str(p) for p in v) if isinstance(v, tuple) else str(v)
+    except Exception:  # noqa: BLE001
+        ver = None
+    env = {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}
+    return {"version": ver, "env": env}
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks with
+    torch.distributed.run on this node (127.0.0.1) and relay rank 0's line."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have}",
+              file=sys.stderr)
+        return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -237,6 +294,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.share_gpu:
         local = 0          # test mode: all ranks on one GPU, gloo moves the bytes
     torch.cuda.set_device(local)
@@ -313,16 +372,14 @@ def run_ours(args):
         # counter), decode
         launches_per_step = 8
     else:
-        comm = coll.Communicator.from_process_group()
-        comm.use_p2p = args.transport == "p2p"
-        if comm.use_p2p:
-            comm.use_p2p = _preflight_p2p(comm, coll, dev)
+        comm = setup_comm(args, dev)
 
         def step(rec=False):
             return coll.zip_all_gather(comm, shard)
-        # codebook+encode leg (6, as at N=1) + decoder init + batched decode; the peer-memory
-        # path adds wait-done, signal-ready, wait-ready, signal-done kernels
-        launches_per_step = 12 if comm.use_p2p else 8
+        # codebook+encode leg (6, as at N=1) + decoder init + decode, plus
+        # p2p: error-word init, done-wait, publish, finish (done flags);
+        # msg: error-word init, size packing, error mapping; generic: as N=1
+        launches_per_step = {"p2p": 12, "msg": 11, "generic": 8}[comm.bench_plane]
 
     # correctness gate before timing: bit-exact round trip
     err = step()
@@ -395,24 +452,55 @@ def run_ours(args):
     value = total_bytes / (ms / 1e3) / 1e9
     raw = None
     if world > 1:
-        # the plain uncompressed collective on the same shards, same run
-        for _ in range(args.warmup):
-            coll.reference_all_gather(comm, shard)
-        torch.cuda.synchronize()
-        dist.barrier()
-        r0 = torch.cuda.Event(enable_timing=True)
-        r1 = torch.cuda.Event(enable_timing=True)
-        r0.record(stream)
-        for _ in range(args.steps):
-            coll.reference_all_gather(comm, shard)
-        r1.record(stream)
-        torch.cuda.synchronize()
-        rt = torch.tensor([r0.elapsed_time(r1) / args.steps], device=dev)
-        dist.all_reduce(rt, op=dist.ReduceOp.MAX)
-        raw_ms = float(rt.item())
+        # deferred decode errors of the timed steps, then one bit-exact check
+        if comm.bench_plane != "generic":
+            comm.native.check()
+        got = coll.zip_all_gather(comm, shard)
+        expect = torch.empty(world * n, dtype=torch.bfloat16, device=dev)
+        dist.all_gather_into_tensor(expect, shard)
+        assert torch.equal(got.view(torch.int16), expect.view(torch.int16)), "all-gather differs"
+        if comm.bench_plane != "generic":
+            comm.native.check()
+
+        def timed(fn):
+            for _ in range(args.warmup):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            tt = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt.item())
+
+        # the plain uncompressed collective on the same shards, same run: a
+        # bare NCCL all-gather (no count agreement, no copies)
+        raw_out = torch.empty(world * n, dtype=torch.bfloat16, device=dev)
+        raw_ms = timed(lambda: dist.all_gather_into_tensor(raw_out, shard))
+        per_rank = 2 * n
+
+        def bw(t_ms):
+            algbw = world * per_rank / (t_ms / 1e3) / 1e9
+            return {"algbw_GBps": algbw, "busbw_GBps": algbw * (world - 1) / world,
+                    "busbw_frac_of_900": algbw * (world - 1) / world / 900.0}
+        planes = {comm.bench_plane: ms}
+        if comm.bench_plane == "p2p":          # the other native plane, for the record
+            comm.native.plane = "msg"
+            try:
+                planes["msg"] = timed(lambda: coll.zip_all_gather(comm, shard))
+            finally:
+                comm.native.plane = "p2p"
+            comm.native.check()
         raw = {"value": total_bytes / (raw_ms / 1e3) / 1e9, "ms_per_step": raw_ms,
-               "backend": args.backend,
-               "transport": "p2p" if getattr(comm, "use_p2p", False) else "nccl",
+               "what": f"torch.distributed.all_gather_into_tensor ({args.backend}) of the same "
+                       "shards",
+               **bw(raw_ms), "zip": {"ms_per_step": ms, **bw(ms)},
+               "zip_planes_ms": planes, "nccl": nccl_info(),
+               "plane": comm.bench_plane, "planes_tried": comm.bench_tried,
                "speedup_zip_over_raw": raw_ms / ms}
 
     # ---- roofline of the dominant kernel -------------------------------------
@@ -546,6 +634,9 @@ def run_ours(args):
         host = shard.cpu().pin_memory()
         e_steps = max(2, min(args.steps, 5))
 
+        if comm.bench_plane != "generic":
+            comm.native.sync_errors = True     # the public API's synchronous error check
+
         def api_step():
             return coll.zip_all_gather(comm, host.to(dev, non_blocking=True))
         res = None
@@ -563,7 +654,7 @@ def run_ours(args):
         del res
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
         e_ms = float(el.item())
-        d2h = 4 * (world - 1) + (4 if comm.use_p2p else 8 * world)
+        d2h = 4 * world + (8 * world if comm.bench_plane == "msg" else 0)
         e2e = {"value": total_bytes / (e_ms / 1e3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
                "note": "per rank: H2D of the shard from pinned memory + zip_all_gather through "
@@ -661,9 +752,7 @@ def run_grad_mix(args):
                     "(the switcher then picks the raw collective)"}), flush=True)
 
 
-def run_moe_a2a(args):
-    """BASELINE configs[2]: MoE dispatch + combine all-to-all, hidden 4096,
-    top-k 8, T tokens per rank, uniform routing; compressed vs plain."""
+def _init_dist(args):
     import torch
     import torch.distributed as dist
     world, rank, local = dist_env()
@@ -675,29 +764,66 @@ def run_moe_a2a(args):
         dist.init_process_group("nccl", device_id=dev)
     else:
         dist.init_process_group(args.backend)
+    return world, rank, local, dev
+
+
+def run_moe_a2a(args):
+    """BASELINE configs[2]: Qwen3-MoE-style expert-parallel dispatch + combine,
+    hidden 4096, 8 experts per GPU, top-k 8, T tokens per rank, uniform or
+    Zipf-skewed routing; compressed (native engine) vs torch's NCCL
+    all_to_all_single of the same splits, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    world, rank, local, dev = _init_dist(args)
     from paper_2604_27844_b200 import collectives as coll
-    comm = coll.Communicator.from_process_group()
-    comm.use_p2p = args.transport == "p2p" and _preflight_p2p(comm, coll, dev)
+    comm = setup_comm(args, dev)
     hidden, topk, T = 4096, 8, args.tokens
-    rows = T * topk
-    per = rows // world
-    g = torch.Generator(device=dev).manual_seed(rank)
-    x = torch.randn(rows * hidden, device=dev, generator=g).to(torch.bfloat16)
-    chunks = [x[q * per * hidden:(q + 1) * per * hidden] for q in range(world)]
-    spec = coll.AlltoAllSpec(chunks, [per * hidden] * world)
+    experts = 8 * world
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    # routing: token -> top-k distinct experts; expert e lives on rank e // 8
+    if args.routing == "zipf":
+        w = 1.0 / torch.arange(1, experts + 1, device=dev, dtype=torch.float64) ** 1.1
+    else:
+        w = torch.ones(experts, device=dev, dtype=torch.float64)
+    choice = torch.multinomial(w.expand(T, experts), topk, replacement=False, generator=g)
+    dest = (choice // 8).flatten()
+    counts_t = torch.bincount(dest, minlength=world)
+    send_rows = counts_t.tolist()
+    rows_all = torch.empty(world * world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(rows_all, counts_t)
+    recv_rows = rows_all.view(world, world)[:, rank].tolist()
+    x = torch.randn(T * topk * hidden, device=dev, generator=g).to(torch.bfloat16)
+    send_counts = [r * hidden for r in send_rows]
+    recv_counts = [r * hidden for r in recv_rows]
+    if comm.bench_plane != "generic":
+        per_peer = max(send_counts + recv_counts)
+        comm.native.reserve(int(1.05 * world * (2.4 * per_peer + 4096)))
+
+    def views(buf, counts):
+        offs = [0]
+        for c in counts:
+            offs.append(offs[-1] + c)
+        return [buf[offs[q]:offs[q + 1]] for q in range(world)]
+
+    spec = coll.AlltoAllSpec(views(x, send_counts), recv_counts)
+    back_spec_counts = send_counts
 
     def zip_step():
-        got = coll.zip_all_to_all_d2(comm, spec)                    # dispatch
-        back = coll.AlltoAllSpec(got, [per * hidden] * world)
-        return coll.zip_all_to_all_d2(comm, back)                   # combine
+        got = coll.zip_all_to_all_d2(comm, spec)                            # dispatch
+        return coll.zip_all_to_all_d2(comm, coll.AlltoAllSpec(got, back_spec_counts))  # combine
+
+    recv_buf = torch.empty(sum(recv_counts), dtype=torch.bfloat16, device=dev)
+    back_buf = torch.empty_like(x)
 
     def raw_step():
-        got = coll.reference_all_to_all(comm, spec)
-        return coll.reference_all_to_all(comm, coll.AlltoAllSpec(got, [per * hidden] * world))
+        dist.all_to_all_single(recv_buf, x, recv_counts, send_counts)
+        dist.all_to_all_single(back_buf, recv_buf, send_counts, recv_counts)
 
     res = zip_step()
+    if comm.bench_plane != "generic":
+        comm.native.check()
     ok = all(torch.equal(a.view(torch.int16), b.view(torch.int16))
-             for a, b in zip(res, [c.view(torch.int16) for c in chunks]))
+             for a, b in zip(res, spec.send_chunks))
     assert ok, "combine(dispatch(x)) != x"
     ms = {}
     for name, fn in (("zip", zip_step), ("raw", raw_step)):
@@ -714,16 +840,24 @@ def run_moe_a2a(args):
         t = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms[name] = float(t.item())
-    send_bytes = 2 * rows * hidden * 2                             # dispatch + combine, per rank
+    if comm.bench_plane != "generic":
+        comm.native.check()
+    send_bytes = 2 * 2 * x.numel()                    # dispatch + combine, this rank
+    tot = torch.tensor([send_bytes], device=dev, dtype=torch.float64)
+    dist.all_reduce(tot)
     if rank == 0:
+        algbw = float(tot.item()) / world / (ms["zip"] / 1e3) / 1e9
         print(json.dumps({
-            "metric": METRIC, "workload": "c3 qwen3-moe dispatch+combine all-to-all",
+            "metric": METRIC, "workload": f"c3 qwen3-moe dispatch+combine all-to-all "
+                                          f"({args.routing} routing)",
             "n_gpus": world, "tokens_per_rank": T, "topk": topk, "hidden": hidden,
-            "value": world * send_bytes / (ms["zip"] / 1e3) / 1e9, "unit": "GB/s",
-            "ms_per_step": ms["zip"], "raw_ms_per_step": ms["raw"],
-            "raw_value": world * send_bytes / (ms["raw"] / 1e3) / 1e9,
-            "speedup_zip_over_raw": ms["raw"] / ms["zip"],
-            "transport": "p2p" if comm.use_p2p else "nccl", "backend": args.backend}), flush=True)
+            "experts": experts, "value": float(tot.item()) / (ms["zip"] / 1e3) / 1e9,
+            "unit": "GB/s", "ms_per_step": ms["zip"], "raw_ms_per_step": ms["raw"],
+            "raw_value": float(tot.item()) / (ms["raw"] / 1e3) / 1e9,
+            "algbw_GBps": algbw, "busbw_GBps": algbw * (world - 1) / world,
+            "speedup_zip_over_raw": ms["raw"] / ms["zip"], "plane": comm.bench_plane,
+            "raw": "torch.distributed.all_to_all_single (NCCL), same splits",
+            "nccl": nccl_info(), "backend": args.backend}), flush=True)
     dist.destroy_process_group()
 
 
@@ -746,14 +880,17 @@ def run_sweep(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2604_27844_b200 import engine, switcher
+    policy = None
     if world > 1:
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(args.backend)
+        world, rank, local, dev = _init_dist(args)
         from paper_2604_27844_b200 import collectives as coll
-        comm = coll.Communicator.from_process_group()
-        comm.use_p2p = args.transport == "p2p" and _preflight_p2p(comm, coll, dev)
+        comm = setup_comm(args, dev)
+        if comm.bench_plane != "generic":
+            comm.native.sync_errors = True
+        # the adaptive switch, fitted ONCE on three sizes with the measured e
+        # (switcher.profile_variants), then asked at every sweep size
+        policy = switcher.profile_variants(comm, "all_gather", sizes=[1 << 16, 1 << 22, 1 << 26],
+                                           trials=3)
     sizes = [(64 << 10) << k for k in range(15)]                # 64 KiB .. 1 GiB
     rows = []
     g = torch.Generator(device=dev).manual_seed(rank)
@@ -808,27 +945,40 @@ def run_sweep(args):
                 t = torch.tensor([a.elapsed_time(b) / reps], device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 return float(t.item())
-            t_zip = timed(lambda: coll.zip_all_gather(comm, x))
-            t_raw = timed(lambda: coll.reference_all_gather(comm, x))
-            rows.append({"bytes": nbytes, "zip_ms": t_zip, "raw_ms": t_raw,
-                         "zip_GBps": world * nbytes / (t_zip / 1e3) / 1e9,
-                         "raw_GBps": world * nbytes / (t_raw / 1e3) / 1e9})
+            raw_out = torch.empty(world * n, dtype=torch.bfloat16, device=dev)
+            t_raw = timed(lambda: dist.all_gather_into_tensor(raw_out, x))
+            row = {"bytes": nbytes, "raw_ms": t_raw,
+                   "raw_GBps": world * nbytes / (t_raw / 1e3) / 1e9}
+            for plane, _ in policy.models:
+                with switcher._variant(comm, plane):
+                    t = timed(lambda: coll.zip_all_gather(comm, x))
+                row[f"zip_{plane}_ms"] = t
+                row[f"zip_{plane}_GBps"] = world * nbytes / (t / 1e3) / 1e9
+            best = min([("native", t_raw)] + [(v, row[f"zip_{v}_ms"]) for v, _ in policy.models],
+                       key=lambda kv: kv[1])
+            path, variant = switcher._decide(comm, policy, nbytes, w, True)
+            t_sw = timed(lambda: switcher.switched_all_gather(comm, x, policy))
+            row.update({"best_measured": best[0],
+                        "switch": variant if path is switcher.Path.ZIPPED else "native",
+                        "switched_ms": t_sw,
+                        "switched_GBps": world * nbytes / (t_sw / 1e3) / 1e9})
+            if nbytes in (1 << 20, 1 << 26):
+                # incompressible gradient mix (C4 outliers): the switch must go native
+                mix = _gpu_mix("mix_x1000", n, dev)
+                path_m, _ = switcher._decide(comm, policy, nbytes, engine.words_view(mix), True)
+                row["outlier_mix_switch"] = path_m.value
+            rows.append(row)
         del x, w
     line = {"metric": METRIC, "workload": "c5 message-size sweep 64 KiB .. 1 GiB per rank",
             "n_gpus": world, "unit": "GB/s", "data": "synthetic N(0, 0.02^2) BF16",
             "rows": rows}
     if world > 1:
-        ds = [r["bytes"] for r in rows]
-        e = 1 / 1.4244          # frame / raw bytes of N(0, 0.02^2) BF16
-        model = switcher.fit_cost_model(ds, [r["raw_ms"] for r in rows],
-                                        [r["zip_ms"] for r in rows], e=e)
-        line["cost_model"] = {"alpha_native_ms": model.alpha_rs, "beta_native_ms_per_B": model.beta_rs,
-                              "alpha_zipped_ms": model.alpha_a2a,
-                              "beta_zipped_ms_per_B": model.beta_a2a, "e": e}
-        for r in rows:
-            r["switcher"] = switcher.select(model, r["bytes"]).value
-            r["best"] = "zipped" if r["zip_ms"] < r["raw_ms"] else "native"
-        line["transport"] = "p2p" if comm.use_p2p else "nccl"
+        line["policy"] = {v: {"alpha_native_s": m.alpha_rs, "beta_native_s_per_B": m.beta_rs,
+                              "alpha_zipped_s": m.alpha_a2a, "beta_zipped_s_per_B": m.beta_a2a,
+                              "e": m.e} for v, m in policy.models}
+        line["switch_agrees_with_best"] = sum(r["switch"] == r["best_measured"] for r in rows)
+        line["plane"] = comm.bench_plane
+        line["nccl"] = nccl_info()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -851,15 +1001,19 @@ def main():
                     help="layer_ag: the headline line (configs[1]); moe_a2a: configs[2]; "
                          "grad_mix: configs[3]; sweep: configs[4]")
     ap.add_argument("--tokens", type=int, default=4096, help="moe_a2a tokens per rank")
+    ap.add_argument("--routing", default="uniform", choices=["uniform", "zipf"],
+                    help="moe_a2a expert routing")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
-                    help="nccl: frames move with NCCL collectives, decode after arrival; "
-                         "p2p: decoder pulls peer frames over NVLink (IPC symmetric buffers)")
+                    help="nccl: the message plane (reference protocols over NCCL); "
+                         "p2p: the decoder pulls peer frames over NVLink (IPC symmetric buffers)")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode: every rank on cuda:0 (use with --backend gloo)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "grad_mix":
