@@ -163,6 +163,110 @@ int zc_signal_peers(void* const* peer_flags, int world, int my_rank, uint64_t ep
 int zc_wait_signals(const void* flags, int world, int my_rank, uint64_t epoch,
                     int64_t timeout_ns, int32_t* err_dev, void* stream);
 
+/* ---- ratio estimate (adaptive switch) ----------------------------------------
+ * Estimated frame bytes / raw bytes of compressing x[0, n) under the codebook
+ * codebook_for would pick (sampled; at least 2^22 words, at most 1/64 of the
+ * bytes): out_dev[0] = e, [1] = sample sigma, [2] = sample escape fraction.
+ * Feeds the message-adaptive switch (switcher.select with the message's e;
+ * reference switcher.py:83-95 uses one profiled e).  ws >= 4096 bytes. */
+int zc_estimate_ratio(const uint16_t* x, int64_t n, void* ws, double* out_dev, void* stream);
+
+/* ---- fused decode + fp32 reduction (reduce-scatter) ---------------------------
+ * Replaces collectives._reduce_chunks over decoded peer chunks
+ * (collectives.py:137-144, :328-341; narrowing bf16.from_float32, bf16.py:53-66):
+ * out = sum over sources in list order, float32 adds with numpy's x86 NaN
+ * semantics, then RNE with the quiet bit forced (out_f32: the float32 sums).
+ * src_dev: device array of W records of zc_red_src_bytes() bytes each,
+ *   { const uint8_t* stat; const uint8_t* dyn; int64_t dyn_len;
+ *     const uint64_t* ready; int32_t raw; int32_t pad; }
+ * (raw != 0: stat points at n raw words; else a frame of n elements with
+ * 512-element groups, dyn = split zero-exponent section or NULL).
+ * err_dev[W] = 0x7F7F7F7F per valid source, else the failing check. */
+int zc_red_src_bytes(void);
+int64_t zc_reduce_scratch_bytes(int W);
+int zc_reduce_frames(const void* src_dev, int W, int64_t n, void* out, int out_f32,
+                     void* hdr_scratch, int32_t* err_dev, void* stream);
+
+/* ---- native compressed collectives (csrc/zc_coll.cu) ---------------------------
+ * Replace the reference's collectives over its transport seam
+ * (collectives.zip_all_gather :203-227, zip_all_to_all_d1/_d2 :245-325,
+ * zip_reduce_scatter :328-341, reference_* :97-170; Communicator
+ * transport.py:576-623) with C++ over NCCL and CUDA peer memory.
+ *
+ * A communicator is one rank of a group: zc_comm_init bootstraps it from an
+ * NCCL unique id (rank 0 calls zc_nccl_get_id and distributes the bytes, as
+ * with ncclCommInitRank); zc_comm_init_local creates all ranks of an
+ * in-process group (one host thread drives each rank afterwards).  Every
+ * rank owns a symmetric buffer (2 frame slots of slot_bytes + flags) that
+ * its peers map (CUDA IPC / direct pointers); when all mappings succeed the
+ * peer-memory plane is available.
+ *
+ * Collective calls are stream-ordered on `stream` and do not synchronise
+ * with the host on the peer-memory plane; the message plane reads the frame
+ * sizes back (the reference's size phase).  err_dev[world] (int32, device)
+ * receives 0x7F7F7F7F per peer whose frame decoded, else the failing check
+ * (engine.ERR_FIELDS; 19 = element count differs, 20 = peer never ready).
+ * book_dev: uint8[8] codebook on the device, or NULL for codebook_for
+ * semantics (sigma measured over the chunks sent).
+ * Status: 0 ok, -1 bad argument, -3 frame too large (UnrepresentableError),
+ * -4 sizes/counts disagree (ProtocolError), -5 peer-memory region too small
+ * for this all-to-all (grow with zc_comm_reserve), -6 transport failure,
+ * -7 a peer's frame is unusable (CollectiveError; zc_comm_last_error gives
+ * the message and the peer), > 0 a cudaError_t. */
+typedef struct zc_comm zc_comm;
+
+#define ZC_PLANE_P2P 1      /* peer-memory plane (default when available) */
+#define ZC_PLANE_MSG 2      /* message plane: reference protocols over NCCL */
+#define ZC_A2A_D1 4         /* all-to-all design 1 (metadata + frames), message plane */
+#define ZC_CHECK_COUNTS 8   /* agree element counts first (NCCL cannot detect mismatches) */
+#define ZC_PIPELINE 16      /* message-plane all-gather: ring steps, per-peer decode on a side stream */
+#define ZC_COMM_NO_P2P 1    /* zc_comm_init flags: never use the peer-memory plane */
+
+int zc_nccl_id_bytes(void);
+int zc_nccl_get_id(void* id_out);
+/* rank of world over NCCL; device = the current CUDA device.  slot_bytes:
+ * peer-memory slot capacity (<= 0: 256 MiB; all-gather slots grow
+ * collectively, all-to-all regions are slot_bytes / world per peer). */
+int zc_comm_init(zc_comm** comm, const void* nccl_id, int rank, int world, int64_t slot_bytes,
+                 int flags);
+/* world in-process ranks; devices[i] is rank i's CUDA device (NULL: current). */
+int zc_comm_init_local(zc_comm** comms, int world, const int* devices, int64_t slot_bytes,
+                       int flags);
+int zc_comm_destroy(zc_comm* comm);
+/* releases in-process ranks blocked in a rendezvous after a peer failed */
+int zc_comm_abort(zc_comm* comm);
+/* info[5] = rank, world, peer-memory plane available, a peer shares this
+ * device, NCCL-backed */
+int zc_comm_info(zc_comm* comm, int* info);
+const char* zc_comm_last_error(zc_comm* comm, int* peer);
+/* TrafficStats (transport.py:559-573): bytes / messages this rank sent
+ * (synchronises the device to read the peer-memory plane's counters) */
+int zc_comm_stats(zc_comm* comm, uint64_t* bytes_sent, uint64_t* messages);
+/* collectively grow the peer-memory slots (every rank, same value) */
+int zc_comm_reserve(zc_comm* comm, int64_t slot_bytes, void* stream);
+
+/* zip_all_gather: out[p*n ..] = rank p's x (n >= 1 on every rank) */
+int zc_allgather(zc_comm* comm, const uint16_t* x, int64_t n, uint16_t* out,
+                 const uint8_t* book_dev, int32_t* err_dev, int flags, void* stream);
+/* reference_all_gather's data movement: ncclAllGather of the words */
+int zc_allgather_raw(zc_comm* comm, const uint16_t* x, int64_t n, uint16_t* out, void* stream);
+/* zip_all_to_all: x = send chunks back to back (send_counts[world] words,
+ * host array), out = receive chunks back to back (recv_counts[world];
+ * recv_counts[rank] must equal send_counts[rank]).  Peer-memory plane, or
+ * the message plane with design 2 (default) / design 1 (ZC_A2A_D1). */
+int zc_alltoall(zc_comm* comm, const uint16_t* x, const int64_t* send_counts,
+                const int64_t* recv_counts, uint16_t* out, const uint8_t* book_dev,
+                int32_t* err_dev, int flags, void* stream);
+int zc_alltoall_raw(zc_comm* comm, const uint16_t* x, const int64_t* send_counts,
+                    const int64_t* recv_counts, uint16_t* out, int flags, void* stream);
+/* zip_reduce_scatter: x = world shards of `shard` words; out = this rank's
+ * shard reduced over ranks in ascending order (bf16 words, or float32 with
+ * out_f32) by the fused decode + reduce kernel */
+int zc_reduce_scatter(zc_comm* comm, const uint16_t* x, int64_t shard, void* out, int out_f32,
+                      const uint8_t* book_dev, int32_t* err_dev, int flags, void* stream);
+int zc_reduce_scatter_raw(zc_comm* comm, const uint16_t* x, int64_t shard, void* out,
+                          int out_f32, int32_t* err_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

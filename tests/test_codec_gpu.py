@@ -409,3 +409,62 @@ def test_two_host_threads_share_a_stream():
     for t in ts:
         t.join()
     assert results == {0: True, 1: True}
+
+
+def test_collective_c_abi_world1_over_nccl():
+    """The collective C-ABI exactly as a non-Python integrator drives it:
+    NCCL unique id -> zc_comm_init -> zc_allgather / zc_alltoall /
+    zc_reduce_scatter (+ raw twins) on device pointers, W = 1."""
+    import ctypes
+    from paper_2604_27844_b200._lib import i64s, lib
+    L = lib()
+    nb = L.zc_nccl_id_bytes()
+    uid = (ctypes.c_uint8 * nb)()
+    assert L.zc_nccl_get_id(uid) == 0
+    comm = ctypes.c_void_p()
+    torch.cuda.set_device(0)
+    assert L.zc_comm_init(ctypes.byref(comm), uid, 0, 1, 1 << 24, 0) == 0
+    try:
+        info = (ctypes.c_int * 5)()
+        assert L.zc_comm_info(comm, info) == 0 and list(info)[:2] == [0, 1] and info[4] == 1
+        words = zo.gaussian(50_001, 0.02, 11)
+        x = torch.from_numpy(words.view(np.int16)).cuda()
+        out = torch.empty_like(x)
+        err = torch.empty(1, dtype=torch.int32, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        assert L.zc_allgather(comm, x.data_ptr(), x.numel(), out.data_ptr(), None,
+                              err.data_ptr(), 0, st) == 0
+        assert torch.equal(out, x) and int(err.item()) == 0x7F7F7F7F
+        out.zero_()
+        assert L.zc_allgather_raw(comm, x.data_ptr(), x.numel(), out.data_ptr(), st) == 0
+        assert torch.equal(out, x)
+        out.zero_()
+        cnt = i64s([x.numel()])
+        assert L.zc_alltoall(comm, x.data_ptr(), cnt, cnt, out.data_ptr(), None, err.data_ptr(),
+                             0, st) == 0
+        assert torch.equal(out, x)
+        rs = torch.empty(50_000, dtype=torch.float32, device="cuda")
+        assert L.zc_reduce_scatter(comm, x.data_ptr(), 50_000, rs.data_ptr(), 1, None,
+                                   err.data_ptr(), 0, st) == 0
+        assert np.array_equal(rs.cpu().numpy().view(np.uint32),
+                              zo.to_f32(words[:50_000]).view(np.uint32))
+        b, m = ctypes.c_uint64(), ctypes.c_uint64()
+        assert L.zc_comm_stats(comm, ctypes.byref(b), ctypes.byref(m)) == 0
+        assert b.value == 0                          # nothing leaves a 1-rank group
+        # mismatched self counts are an argument error, not a hang
+        assert L.zc_alltoall(comm, x.data_ptr(), cnt, i64s([7]), out.data_ptr(), None,
+                             err.data_ptr(), 0, st) == -1
+    finally:
+        L.zc_comm_destroy(comm)
+
+
+def test_zbf16_round_trip(tmp_path):
+    # reference tests/test_container.py:172-179, plus the file bytes against the oracle
+    data = gaussian_words(1234, seed=8)
+    chunk = zc.compress(data, zc.derive_codebook(1.0))
+    path = tmp_path / "x.zbf16"
+    nbytes = container.write_zbf16(path, chunk)
+    assert path.stat().st_size == nbytes
+    assert path.read_bytes() == zo.encode(data, zc.derive_codebook(1.0).entries)
+    back = zc.decompress(container.read_zbf16(path))
+    assert np.array_equal(back.cpu().numpy().view(np.uint16), data)
