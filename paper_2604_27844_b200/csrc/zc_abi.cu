@@ -4,6 +4,8 @@
 #include <cstring>
 #include <mutex>
 #include <vector>
+#include <nvtx3/nvToolsExt.h>
+
 #include "zc_common.cuh"
 
 namespace zc {
@@ -61,6 +63,11 @@ constexpr int kStatusTooLarge = -3;
 int64_t tiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
 
 int status_of(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
+
+struct Range {   // NVTX range around each codec entry point (header-only NVTX v3)
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
 }  // namespace
 
 
@@ -124,6 +131,7 @@ int64_t zc_workspace_bytes(int64_t total_elems, int nseg) {
 int zc_codebook_measured(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n, int nseg,
                          void* ws, int64_t ws_bytes, uint8_t* book_dev, double* result_dev,
                          int flags, cudaStream_t stream) {
+  Range nvtx_range("zc_codebook_measured");
   if (nseg < 0 || nseg > kMaxSegments || !book_dev || !result_dev || !ws) return kStatusBadArg;
   StatSegs s{};
   int k = 0;
@@ -147,6 +155,7 @@ int zc_codebook_measured(const uint16_t* x, const int64_t* seg_off, const int64_
 
 int zc_codebook_modal(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n, int nseg,
                       void* ws, int64_t ws_bytes, uint8_t* book_dev, cudaStream_t stream) {
+  Range nvtx_range("zc_codebook_modal");
   if (nseg < 0 || nseg > kMaxSegments || !book_dev || !ws) return kStatusBadArg;
   StatSegs s{};
   int k = 0;
@@ -170,6 +179,7 @@ int zc_encode(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
               const int64_t* frame_off, int nseg, const uint8_t* book_dev, int gs_log2,
               uint8_t* frames, void* ws, int64_t ws_bytes, uint64_t* frame_len_dev,
               cudaStream_t stream) {
+  Range nvtx_range("zc_encode");
   if (nseg < 1 || nseg > kMaxSegments || !x || !book_dev || !frames || !ws || !frame_len_dev)
     return kStatusBadArg;
   if (gs_log2 < 0 || gs_log2 > 30) return kStatusBadArg;
@@ -194,6 +204,7 @@ int zc_encode_measured(const uint16_t* x, const int64_t* seg_off, const int64_t*
                        const int64_t* frame_off, int nseg, int gs_log2, uint8_t* frames, void* ws,
                        int64_t ws_bytes, uint64_t* frame_len_dev, uint8_t* book_dev,
                        double* result_dev, int flags, cudaStream_t stream) {
+  Range nvtx_range("zc_encode_measured");
   if (nseg < 1 || nseg > kMaxSegments || !x || !book_dev || !result_dev || !frames || !ws ||
       !frame_len_dev)
     return kStatusBadArg;
@@ -224,6 +235,7 @@ int zc_encode_measured(const uint16_t* x, const int64_t* seg_off, const int64_t*
 int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64_t* dyn_len,
               const int64_t* n, const int64_t* out_off, int nseg, uint16_t* out, int32_t* err_dev,
               void* ws, int64_t ws_bytes, int write_out, cudaStream_t stream) {
+  Range nvtx_range("zc_decode");
   if (nseg < 1 || nseg > kMaxSegments || !stat || !dyn || !n || !err_dev || !ws) return kStatusBadArg;
   if ((write_out & 1) && (!out || !out_off)) return kStatusBadArg;
   DecodeSegs s{};
@@ -246,6 +258,7 @@ int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64
 
 int zc_decode_groups(const uint8_t* frame, int64_t n, int gs_log2, int64_t g0, int64_t g1,
                      uint16_t* out, cudaStream_t stream) {
+  Range nvtx_range("zc_decode_groups");
   if (!frame || !out || n < 1 || gs_log2 < 0 || gs_log2 > 30) return kStatusBadArg;
   if ((reinterpret_cast<uintptr_t>(frame) & 7) != 0) return kStatusBadArg;
   const int64_t groups = (n + (int64_t(1) << gs_log2) - 1) >> gs_log2;

@@ -42,6 +42,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "zc_common.cuh"
 
 namespace zc {
@@ -66,6 +68,14 @@ extern "C" int64_t zc_workspace_bytes(int64_t total_elems, int nseg);
 using namespace zc;
 
 namespace {
+
+// NVTX range around every collective call (host enqueue side): a profiler
+// timeline shows each rank's encode / publish / decode launches under the
+// collective that issued them (SURVEY §5 tracing).  Header-only NVTX v3.
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
 
 constexpr int kStatusBadArg = -1;
 constexpr int kStatusProtocol = -4;    // sizes / counts disagree (ProtocolError)
@@ -1323,6 +1333,7 @@ static bool use_p2p(zc_comm* c, int flags) {
 
 int zc_allgather(zc_comm* c, const uint16_t* x, int64_t n, uint16_t* out, const uint8_t* book_dev,
                  int32_t* err_dev, int flags, void* stream) {
+  Range nvtx_range("zc_allgather");
   if (!c || n < 1 || !x || !out) return kStatusBadArg;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   c->last_error.clear();
@@ -1336,6 +1347,7 @@ int zc_allgather(zc_comm* c, const uint16_t* x, int64_t n, uint16_t* out, const 
 }
 
 int zc_allgather_raw(zc_comm* c, const uint16_t* x, int64_t n, uint16_t* out, void* stream) {
+  Range nvtx_range("zc_allgather_raw");
   if (!c || n < 0 || (n && (!x || !out))) return kStatusBadArg;
   c->host_bytes += (uint64_t)(2 * n) * (c->world - 1);
   c->host_msgs += (uint64_t)(c->world - 1);
@@ -1345,6 +1357,7 @@ int zc_allgather_raw(zc_comm* c, const uint16_t* x, int64_t n, uint16_t* out, vo
 int zc_alltoall(zc_comm* c, const uint16_t* x, const int64_t* send_counts,
                 const int64_t* recv_counts, uint16_t* out, const uint8_t* book_dev,
                 int32_t* err_dev, int flags, void* stream) {
+  Range nvtx_range("zc_alltoall");
   if (!c || !send_counts || !recv_counts) return kStatusBadArg;
   for (int p = 0; p < c->world; ++p)
     if (send_counts[p] < 0 || recv_counts[p] < 0) return kStatusBadArg;
@@ -1365,6 +1378,7 @@ int zc_alltoall(zc_comm* c, const uint16_t* x, const int64_t* send_counts,
 
 int zc_alltoall_raw(zc_comm* c, const uint16_t* x, const int64_t* send_counts,
                     const int64_t* recv_counts, uint16_t* out, int flags, void* stream) {
+  Range nvtx_range("zc_alltoall_raw");
   if (!c || !send_counts || !recv_counts) return kStatusBadArg;
   if (send_counts[c->rank] != recv_counts[c->rank]) return kStatusBadArg;
   c->last_error.clear();
@@ -1374,6 +1388,7 @@ int zc_alltoall_raw(zc_comm* c, const uint16_t* x, const int64_t* send_counts,
 
 int zc_reduce_scatter(zc_comm* c, const uint16_t* x, int64_t shard, void* out, int out_f32,
                       const uint8_t* book_dev, int32_t* err_dev, int flags, void* stream) {
+  Range nvtx_range("zc_reduce_scatter");
   if (!c || shard < 1 || !x || !out) return kStatusBadArg;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   c->last_error.clear();
@@ -1391,6 +1406,7 @@ int zc_reduce_scatter(zc_comm* c, const uint16_t* x, int64_t shard, void* out, i
 
 int zc_reduce_scatter_raw(zc_comm* c, const uint16_t* x, int64_t shard, void* out, int out_f32,
                           int32_t* err_dev, void* stream) {
+  Range nvtx_range("zc_reduce_scatter_raw");
   if (!c || shard < 1 || !x || !out) return kStatusBadArg;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int W = c->world, me = c->rank;
