@@ -719,7 +719,7 @@ def run_grad_mix(args):
         flen = torch.empty(1, dtype=torch.int64, device=dev)
         err = torch.empty(1, dtype=torch.int32, device=dev)
         enc = lambda: engine.encode_measured(w, [(0, n)], 9, frames, [0], flen)  # noqa: E731
-        dec = lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err)  # noqa: E731
+        dec = lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err, groups512=True)  # noqa: E731
         enc()
         dec()
         torch.cuda.synchronize()
@@ -907,14 +907,18 @@ def run_sweep(args):
 
             def step():
                 engine.encode_measured(w, [(0, n)], 9, frames, [0], flen)
-                engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err)
+                engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err, groups512=True)
             step()
             torch.cuda.synchronize()
             assert int(err.item()) == engine.ERR_OK and torch.equal(out, w)
             F = int(flen.item())
+            # several steps per graph: the host's graph-launch rate (~5 us)
+            # would otherwise be what small messages measure
+            inner = max(1, min(20, (64 << 20) // nbytes))
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr):
-                step()
+                for _ in range(inner):
+                    step()
             for _ in range(3):
                 gr.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -924,7 +928,7 @@ def run_sweep(args):
                 gr.replay()
             b.record()
             torch.cuda.synchronize()
-            ms = a.elapsed_time(b) / reps
+            ms = a.elapsed_time(b) / reps / inner
             ratio = 2 * n / F
             saved = nbytes * (1 - 1 / ratio)
             rows.append({"bytes": nbytes, "codec_ms": ms, "codec_GBps": nbytes / (ms / 1e3) / 1e9,

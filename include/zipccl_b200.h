@@ -121,8 +121,13 @@ int zc_encode_measured(const uint16_t* x, const int64_t* seg_off, const int64_t*
  * section (-1 unknown; host array may be NULL), n[i] = expected element count,
  * out_off[i] = element offset of the output.  err_dev[i] = 0x7F7F7F7F when the
  * frame is valid, else the smallest failing check in reference order
- * (see engine.ERR_FIELDS).  write_out = 0 validates only (reference
- * CompressedChunk.validate, codec.py:252-255). */
+ * (see engine.ERR_FIELDS).  write_out bit 0 clear validates only (reference
+ * CompressedChunk.validate, codec.py:252-255); bit 1: frames may use groups
+ * larger than 4096 elements; bit 3 (ZC_DECODE_GROUPS512): the caller knows
+ * every frame uses 512-element groups, so frames of at most 512 Ki elements
+ * are decoded by one cluster launch (a frame with another group size then
+ * fails with code 22). */
+#define ZC_DECODE_GROUPS512 8
 int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64_t* dyn_len,
               const int64_t* n, const int64_t* out_off, int nseg, uint16_t* out,
               int32_t* err_dev, void* ws, int64_t ws_bytes, int write_out, void* stream);

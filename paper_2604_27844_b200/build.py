@@ -18,7 +18,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libzipccl_b200.so"
 SOURCES = ["zc_abi.cu", "zc_encode.cu", "zc_decode.cu", "zc_stats.cu", "zc_p2p.cu",
-           "zc_reduce.cu", "zc_coll.cu", "zc_estimate.cu"]
+           "zc_reduce.cu", "zc_coll.cu", "zc_estimate.cu",
+           "zc_small.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -461,7 +461,8 @@ def _run_decode(chunk: CompressedChunk, write_out: bool, exc, out=None):
     if write_out and out is None:
         out = torch.empty(n, dtype=torch.int16, device=frame.device)
     err = engine.decode([frame.data_ptr()], [0], None, [n], out, [0] if out is not None else None,
-                        write_out=write_out, large_groups=chunk.group_size > engine.TILE)
+                        write_out=write_out, large_groups=chunk.group_size > engine.TILE,
+                        groups512=chunk.group_size == 512)
     code = int(err[0].item())
     if code != engine.ERR_OK:
         raise exc(engine.err_message(code))

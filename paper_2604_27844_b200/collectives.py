@@ -246,7 +246,7 @@ def zip_all_gather(comm: Communicator, local, sigma: float | None = None) -> tor
     err = engine.decode([static.data_ptr() + p * S for p in peers],
                         [dyn.data_ptr() + int(doff[p]) for p in peers],
                         [dyn_lens[p] for p in peers], [n] * len(peers), out,
-                        [p * n for p in peers])
+                        [p * n for p in peers], groups512=True)
     out[me * n:(me + 1) * n].copy_(words)
     _raise_decode_errors(err, peers)
     return out
@@ -284,7 +284,7 @@ def _finish_a2a(comm, spec, buf, offs, counts, recv, peers_in, stat_ptrs, dyn_pt
     roffs = np.concatenate([[0], np.cumsum(spec.recv_counts)]).astype(np.int64)
     if peers_in:
         err = engine.decode(stat_ptrs, dyn_ptrs, dyn_lens, out_counts, flat,
-                            [int(roffs[p]) for p in peers_in])
+                            [int(roffs[p]) for p in peers_in], groups512=True)
         _raise_decode_errors(err, peers_in)
     result = [flat[int(roffs[p]):int(roffs[p]) + spec.recv_counts[p]]
               for p in range(comm.world_size)]

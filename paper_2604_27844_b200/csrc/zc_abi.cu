@@ -252,8 +252,9 @@ int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64
     s.tile_start[i + 1] = s.tile_start[i] + tiles_of(n[i]);
   }
   if (128 + 8 * s.tile_start[nseg] > ws_bytes) return kStatusWorkspace;
-  // bits 0-1 only (write / large groups); pull mode is the collectives' own
-  return status_of(launch_decode(s, out, err_dev, ws, write_out & 3, stream));
+  // bits 0, 1, 3 (write / large groups / 512-element groups); pull mode is
+  // the collectives' own
+  return status_of(launch_decode(s, out, err_dev, ws, write_out & 11, stream));
 }
 
 int zc_decode_groups(const uint8_t* frame, int64_t n, int gs_log2, int64_t g0, int64_t g1,

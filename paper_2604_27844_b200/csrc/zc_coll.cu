@@ -61,6 +61,7 @@ cudaError_t preload_decode();
 cudaError_t preload_stats();
 cudaError_t preload_reduce();
 cudaError_t preload_estimate();
+cudaError_t preload_small();
 }  // namespace zc
 
 extern "C" int64_t zc_workspace_bytes(int64_t total_elems, int nseg);
@@ -543,7 +544,7 @@ int p2p_decode(zc_comm* c, const std::vector<int>& peers, const std::vector<int6
     for (auto v : counts) total += v;
     cudaError_t ce = c->ws.need(zc_workspace_bytes(total, nseg) + 4096, st);
     if (ce != cudaSuccess) return (int)ce;
-    ce = launch_decode(s, out, sc.seg_err, c->ws.p, 1 | 4, st);
+    ce = launch_decode(s, out, sc.seg_err, c->ws.p, 1 | 4 | 8, st);
     if (ce != cudaSuccess) return (int)ce;
   }
   finish_kernel<<<1, 64, 0, st>>>(sc.seg_err, seg_rank, nseg, err, c->world, c->rank,
@@ -738,7 +739,7 @@ int decode_local(zc_comm* c, const std::vector<int>& ranks, const std::vector<co
   }
   cudaError_t ce = c->ws.need(zc_workspace_bytes(total, nseg) + 4096, st);
   if (ce != cudaSuccess) return (int)ce;
-  ce = launch_decode(s, out, seg_err, c->ws.p, 1, st);
+  ce = launch_decode(s, out, seg_err, c->ws.p, 1 | 8, st);
   if (ce != cudaSuccess) return (int)ce;
   if (err) map_err_kernel<<<1, 64, 0, st>>>(seg_err, sr, nseg, err, c->world);
   return cuda_status(cudaGetLastError());
@@ -1198,6 +1199,7 @@ static int comm_common_init(zc_comm* c, int64_t slot_bytes) {
   preload_stats();
   preload_reduce();
   preload_estimate();
+  preload_small();
   {
     cudaFuncAttributes a;
     const void* ks[] = {(const void*)publish_kernel, (const void*)wait_flags_kernel,

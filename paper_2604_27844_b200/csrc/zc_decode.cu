@@ -902,8 +902,28 @@ __global__ void decode_init_kernel(int32_t* __restrict__ err, int nseg, unsigned
   if (t <= nseg) counter[t] = 0u;                   // global claim + per-segment (pull) counters
 }
 
+cudaError_t launch_decode_small(const DecodeSegs&, uint16_t*, int32_t*, int, cudaStream_t);
+
+// Frames of at most this many elements (every segment), known to use
+// 512-element groups (flags bit 3), take the one-launch cluster decoder.
+// Its 8 CTAs x 8 warps walk the groups with dependent global loads, so it
+// stays latency-bound beyond ~2 groups per warp (64 Ki words); the ring
+// decoder takes over there (bench.py --workload sweep).
+static int64_t small_decode_max() {
+  static const int64_t v = [] {
+    const char* e = getenv("ZC_SMALL_DEC_MAX_WORDS");
+    return e ? (int64_t)atoll(e) : (int64_t)65536;
+  }();
+  return v;
+}
+
 cudaError_t launch_decode(const DecodeSegs& segs, uint16_t* out, int32_t* err, void* ws,
                           int flags, cudaStream_t st) {
+  if ((flags & 8) && !(flags & 2) && segs.nseg >= 1) {
+    bool small = true;
+    for (int s = 0; s < segs.nseg; ++s) small = small && segs.n[s] <= small_decode_max();
+    if (small) return launch_decode_small(segs, out, err, flags, st);
+  }
   // flags bit 0: write the words; bit 1: frames may use groups larger than a
   // tile (then the look-back decoder is used)
   const int write_out = flags & 1;

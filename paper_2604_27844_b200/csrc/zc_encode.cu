@@ -894,10 +894,17 @@ cudaError_t launch_encode(const uint16_t*, const EncodeSegs&, const uint8_t*, ui
 // so one memset of [0, kLbStatusOff + 8 x tiles) serves a measured encode.
 constexpr int64_t kLbStatusOff = 256 + 8 * 4096;
 
+bool small_encode_ok(int64_t n, int gsl);
+cudaError_t launch_encode_small(const uint16_t*, int64_t, const uint8_t*, uint8_t*, uint64_t*,
+                                uint8_t*, double*, cudaStream_t);
+
 cudaError_t launch_encode(const uint16_t* x, const EncodeSegs& segs, const uint8_t* book,
                           uint8_t* frames, void* ws, uint64_t* frame_len, cudaStream_t st,
                           bool zeroed) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
+  if (segs.nseg == 1 && small_encode_ok(segs.n[0], segs.gs_log2))   // one cluster launch
+    return launch_encode_small(x + segs.x_off[0], segs.n[0], book, frames + segs.frame_off[0],
+                               frame_len, nullptr, nullptr, st);
   uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
   if (ntiles <= kLookbackMaxTiles) {
     unsigned* counter = reinterpret_cast<unsigned*>(w8);
@@ -944,6 +951,9 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
                                uint8_t* book, double* result, int speculative, cudaStream_t st) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
   uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
+  if (segs.nseg == 1 && small_encode_ok(segs.n[0], segs.gs_log2))   // statistic + encode, one launch
+    return launch_encode_small(x + segs.x_off[0], segs.n[0], nullptr, frames + segs.frame_off[0],
+                               frame_len, book, result, st);
   if (!speculative || ntiles < kSpecMinTiles) {
     // small inputs: one memset for the statistic's and the look-back
     // encoder's counters (fewer graph nodes on the latency-bound path)

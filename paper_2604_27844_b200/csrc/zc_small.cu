@@ -1,0 +1,529 @@
+// Small-message fast path: ONE launch for codebook_for + compress and ONE
+// launch for parse + decompress, for messages up to 512 Ki words (1 MiB) with
+// the default 512-element groups (below ~2 MiB the codec was
+// a chain of 5-8 dependent launches, ~23 us of latency for a few us of work).
+//
+// Both kernels run one thread-block cluster (<= 8 CTAs, distributed shared
+// memory) per message:
+//
+// encode_small_kernel (reference codec_for + compress + serialize,
+// codec.py:164-185, :264-305, container.py:65-95): every CTA loads its slice
+// (a multiple of 512 words) into shared memory once, accumulates the exact
+// f64 statistic of its finite elements (numpy's two passes: the mean, then
+// the squared deviations, each summed in a fixed order over lanes, warps and
+// cluster ranks via DSMEM), so EVERY CTA derives the identical codebook (or
+// takes the given one).  A warp encodes one
+// 512-word group from shared memory (lane = 16 words): sign-mantissa bytes,
+// the three plane half-words, the escape mask; the per-group escape counts
+// are scanned inside the CTA, the CTA totals across the cluster over DSMEM,
+// then group_index entries and escape bytes go straight to their final
+// places.  CTA 0 writes header, pads and the frame length.  No global
+// atomics, no memset, no second kernel.
+//
+// decode_small_kernel (container.parse + codec.decompress, container.py:113-180,
+// codec.py:210-327): one cluster per frame (segment); every CTA validates the
+// header, a warp decodes one group straight from global memory (escape base
+// gi[g] + warp scan, consistency gi[g] + escapes(g) == gi[g+1] / zero_count),
+// and the CTAs' first failing check is min-reduced over DSMEM, so CTA 0 writes
+// the error word with a plain store (no init launch).  Pull mode (peer
+// frames, the collectives): thread 0 waits for the segment's ready flag.
+#include <cooperative_groups.h>
+
+#include "zc_common.cuh"
+#include "zc_stats.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace zc {
+
+constexpr int kSmallCtas = 8;                       // portable cluster size
+constexpr int64_t kSmallCtaWords = 65536;           // 128 KB of shared memory per CTA
+constexpr int64_t kSmallMaxWords = kSmallCtas * kSmallCtaWords;
+constexpr int kSmallThreads = kThreads;             // 8 warps (StatAcc block merge)
+
+struct SmallShared {                                 // static part of the encoder's smem
+  double s1, n, q;                                   // this CTA's sums (statistic)
+  int efin;                                          // exponent of a finite element
+  double red[2][kSmallThreads / 32];
+  int ered[kSmallThreads / 32];
+  uint32_t total;                                    // escapes of this CTA
+  uint32_t gcnt[kSmallCtaWords / 512];               // per-group escape counts -> prefix
+  uint8_t code[256];                                 // exponent -> code (0 = escape)
+  uint8_t book[8];
+};
+
+__device__ __forceinline__ void write_header(uint8_t* frame, int64_t n, int64_t zc, int gsl,
+                                             const uint8_t* book, const Layout& L) {
+  uint64_t* h = reinterpret_cast<uint64_t*>(frame);
+  h[0] = 0x4C43435Aull | (1ull << 32) | ((uint64_t)gsl << 48);    // "ZCCL", v1, flags 0
+  h[1] = (uint64_t)n;
+  h[2] = (uint64_t)zc;
+  uint64_t e = 0;
+  for (int i = 0; i < 7; ++i) e |= (uint64_t)book[i] << (8 * i);
+  e |= (uint64_t)book[0] << 56;
+  h[3] = e;
+  uint32_t* offs = reinterpret_cast<uint32_t*>(frame + 32);
+  for (int i = 0; i < 6; ++i) offs[i] = (uint32_t)L.off[i];
+  for (int i = 7; i < 16; ++i) h[i] = 0;           // bytes 56 .. 127
+}
+
+// Block sums of (a, b) in a fixed order (lane tree, then warps in order) and
+// max of e; every thread receives the totals.
+__device__ __forceinline__ void block_sum2(double& a, double& b, int& e,
+                                           double (&red)[2][kSmallThreads / 32]) {
+  __shared__ int s_e[kSmallThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    const int eo = __shfl_xor_sync(0xffffffffu, e, o);
+    e = eo > e ? eo : e;
+  }
+  if (lane == 0) { red[0][warp] = a; red[1][warp] = b; s_e[warp] = e; }
+  __syncthreads();
+  a = 0.0;
+  b = 0.0;
+  e = -1;
+  for (int k = 0; k < kSmallThreads / 32; ++k) {
+    a += red[0][k];
+    b += red[1][k];
+    e = s_e[k] > e ? s_e[k] : e;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void zero_range(uint8_t* p, int64_t a, int64_t b) {
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) p[i] = 0;
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+encode_small_kernel(const uint16_t* __restrict__ x, int64_t n, int64_t wpc,
+                    const uint8_t* __restrict__ book_in, uint8_t* __restrict__ frame,
+                    uint64_t* __restrict__ frame_len, uint8_t* __restrict__ book_out,
+                    double* __restrict__ result) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  uint16_t* words = reinterpret_cast<uint16_t*>(s_dyn);                       // wpc words
+  uint16_t* emask = reinterpret_cast<uint16_t*>(s_dyn + 2 * wpc);            // groups x 32
+  __shared__ SmallShared S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rank = (int)cluster.block_rank(), C = (int)cluster.num_blocks();
+  (void)lane;
+  const int64_t r0 = (int64_t)rank * wpc;
+  const int64_t r1 = r0 + wpc < n ? r0 + wpc : n;
+  const int64_t cnt = r1 > r0 ? r1 - r0 : 0;
+  const Layout L = layout_of(n, 9);
+
+  // ---- 1. slice -> shared memory (TMA bulk copies when 16-B aligned) ------
+  __shared__ __align__(8) uint64_t s_bar;
+  const uint16_t* xs = x + r0;
+  const bool tma = (reinterpret_cast<uintptr_t>(xs) & 15) == 0;
+  const int64_t nbulk = tma ? (cnt * 2) & ~int64_t(15) : 0;      // bytes by TMA
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+    if (nbulk) {
+      mbar_arrive_expect_tx(&s_bar, (uint32_t)nbulk);
+      for (int64_t o = 0; o < nbulk; o += 32768) {
+        const int64_t b = nbulk - o < 32768 ? nbulk - o : 32768;
+        tma_load_1d(reinterpret_cast<uint8_t*>(words) + o, reinterpret_cast<const uint8_t*>(xs) + o,
+                    (uint32_t)b, &s_bar);
+      }
+    } else {
+      mbar_arrive(&s_bar);
+    }
+  }
+  for (int64_t i = nbulk / 2 + tid; i < cnt; i += kSmallThreads) words[i] = xs[i];
+  __syncthreads();
+  mbar_wait(&s_bar, 0);
+
+  // ---- 2. codebook: numpy's two-pass f64 statistic, merged over the cluster
+  // mean = sum(x) / N, then M2 = sum((x - mean)^2) over the finite elements
+  // (bf16.measure_sigma, bf16.py:88-103; np.std is two-pass too), partial
+  // sums added in a fixed order (lane tree, warps, cluster ranks): no
+  // divisions on the serial path, identical on every CTA.
+  if (book_in == nullptr) {
+    double a = 0.0, c = 0.0;
+    int e_fin = -1;
+    for (int64_t i = tid; i < cnt; i += kSmallThreads) {
+      const uint32_t w = words[i];
+      if ((w & 0x7F80u) != 0x7F80u) {
+        a += (double)__uint_as_float(w << 16);
+        c += 1.0;
+        e_fin = (int)((w >> 7) & 0xFF);
+      }
+    }
+    block_sum2(a, c, e_fin, S.red);
+    if (tid == 0) { S.s1 = a; S.n = c; S.efin = e_fin; }
+  }
+  cluster.sync();                                          // sums visible
+  double mean = 0.0, N = 0.0;
+  int ce = -1;
+  if (book_in == nullptr) {
+    double S1 = 0.0;
+    for (int r = 0; r < C; ++r) {                           // rank order
+      const SmallShared* q = cluster.map_shared_rank(&S, r);
+      S1 += q->s1;
+      N += q->n;
+      if (ce < 0) ce = q->efin;
+    }
+    mean = N > 0.0 ? S1 / N : 0.0;
+    double q2 = 0.0, dummy = 0.0;
+    int ed = -1;
+    for (int64_t i = tid; i < cnt; i += kSmallThreads) {
+      const uint32_t w = words[i];
+      if ((w & 0x7F80u) != 0x7F80u) {
+        const double d = (double)__uint_as_float(w << 16) - mean;
+        q2 = fma(d, d, q2);
+      }
+    }
+    block_sum2(q2, dummy, ed, S.red);
+    if (tid == 0) S.q = q2;
+  }
+  cluster.sync();                                          // deviations visible
+  if (tid == 0) {
+    if (book_in == nullptr) {
+      double Q = 0.0;
+      for (int r = 0; r < C; ++r) Q += cluster.map_shared_rank(&S, r)->q;
+      double res[3];
+      finish_codebook(N, Q, ce, n, S.book, res);
+      if (rank == 0) {
+        for (int i = 0; i < 7; ++i) book_out[i] = S.book[i];
+        book_out[7] = 0;
+        result[0] = res[0];
+        result[1] = res[1];
+        result[2] = res[2];
+      }
+    } else {
+      for (int i = 0; i < 7; ++i) S.book[i] = book_in[i];
+    }
+  }
+  __syncthreads();
+  {
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) c = (S.book[i] == tid) ? uint32_t(i + 1) : c;
+    S.code[tid] = (uint8_t)c;
+  }
+  __syncthreads();
+
+  // ---- 3. encode: a warp per 512-word group, 16 words per lane -------------
+  const int64_t groups = (cnt + 511) / 512;
+  for (int64_t g = warp; g < groups; g += kSmallThreads / 32) {
+    const int64_t lb = g * 512 + lane * 16;                 // slice-local
+    const int64_t nv64 = cnt - lb;
+    const int nv = nv64 >= 16 ? 16 : (nv64 > 0 ? (int)nv64 : 0);
+    uint32_t p0 = 0, p1 = 0, p2 = 0, esc = 0, sm[4] = {0, 0, 0, 0};
+    uint32_t wv[8];
+    if (nv == 16) {                                          // 2 x LDS.128
+      const uint4 a = *reinterpret_cast<const uint4*>(words + lb);
+      const uint4 b = *reinterpret_cast<const uint4*>(words + lb + 8);
+      wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
+      wv[4] = b.x; wv[5] = b.y; wv[6] = b.z; wv[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t lo = (2 * j < nv) ? words[lb + 2 * j] : 0u;
+        const uint32_t hi = (2 * j + 1 < nv) ? words[lb + 2 * j + 1] : 0u;
+        wv[j] = lo | (hi << 16);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t w = (wv[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+      const uint32_t c = S.code[(w >> 7) & 0xFF];
+      const uint32_t live = j < nv ? 1u : 0u;
+      p0 |= (c & 1u) << j;
+      p1 |= ((c >> 1) & 1u) << j;
+      p2 |= ((c >> 2) & 1u) << j;
+      esc |= (uint32_t(c == 0) & live) << j;
+      sm[j >> 2] |= (((w >> 8) & 0x80u) | (w & 0x7Fu)) << (8 * (j & 3));
+    }
+    if (nv < 16) {                                           // words past n: no bits
+      const uint32_t vm = nv > 0 ? (1u << nv) - 1u : 0u;
+      p0 &= vm; p1 &= vm; p2 &= vm;
+    }
+    const int64_t e0 = r0 + lb;                             // global element index
+    if (nv == 16) {
+      st_stream_v4(frame + L.off[0] + e0, make_uint4(sm[0], sm[1], sm[2], sm[3]));
+      const int64_t pb = e0 >> 3;
+      *reinterpret_cast<uint16_t*>(frame + L.off[1] + pb) = (uint16_t)p0;
+      *reinterpret_cast<uint16_t*>(frame + L.off[2] + pb) = (uint16_t)p1;
+      *reinterpret_cast<uint16_t*>(frame + L.off[3] + pb) = (uint16_t)p2;
+    } else if (nv > 0) {
+      for (int j = 0; j < nv; ++j) frame[L.off[0] + e0 + j] = (uint8_t)(sm[j >> 2] >> (8 * (j & 3)));
+      const int64_t pb = e0 >> 3;
+      frame[L.off[1] + pb] = (uint8_t)p0;
+      frame[L.off[2] + pb] = (uint8_t)p1;
+      frame[L.off[3] + pb] = (uint8_t)p2;
+      if (nv > 8) {
+        frame[L.off[1] + pb + 1] = (uint8_t)(p0 >> 8);
+        frame[L.off[2] + pb + 1] = (uint8_t)(p1 >> 8);
+        frame[L.off[3] + pb + 1] = (uint8_t)(p2 >> 8);
+      }
+    }
+    emask[g * 32 + lane] = (uint16_t)esc;
+    uint32_t c = __popc(esc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) S.gcnt[g] = c;
+  }
+  __syncthreads();
+  if (warp == 0) {                                          // exclusive prefix of gcnt
+    uint32_t carry = 0;
+    for (int64_t g0 = 0; g0 < groups; g0 += 32) {
+      const uint32_t v = (g0 + lane < groups) ? S.gcnt[g0 + lane] : 0u;
+      const uint32_t inc = warp_incl_scan(v);
+      if (g0 + lane < groups) S.gcnt[g0 + lane] = carry + inc - v;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) S.total = carry;
+  }
+  cluster.sync();                                           // totals visible
+  uint32_t base = 0, zc = 0;
+  for (int r = 0; r < C; ++r) {
+    const uint32_t t = *cluster.map_shared_rank(&S.total, r);
+    if (r < rank) base += t;
+    zc += t;
+  }
+  cluster.sync();                                           // no DSMEM reads after this
+
+  // ---- 4. group_index + escapes at their final places ----------------------
+  uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
+  const int64_t g_first = r0 / 512;
+  for (int64_t g = tid; g < groups; g += kSmallThreads) gi[g_first + g] = base + S.gcnt[g];
+  uint8_t* dyn = frame + L.off[5];
+  for (int64_t g = warp; g < groups; g += kSmallThreads / 32) {
+    const uint32_t m0 = emask[g * 32 + lane];
+    const uint32_t c = __popc(m0);
+    const uint32_t incl = warp_incl_scan(c);
+    if (__ballot_sync(0xffffffffu, m0 != 0) == 0) continue;
+    uint32_t pos = base + S.gcnt[g] + incl - c;
+    uint32_t m = m0;
+    const int64_t lb = g * 512 + lane * 16;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      dyn[pos++] = (uint8_t)((words[lb + j] >> 7) & 0xFF);
+    }
+  }
+
+  // ---- 5. CTA 0: header, pads, frame length --------------------------------
+  if (rank == 0) {
+    if (tid == 0) {
+      write_header(frame, n, zc, 9, S.book, L);
+      *frame_len = (uint64_t)L.off[5] + (uint64_t)pad128(zc);
+    }
+    const int64_t pb = L.plane_bytes;
+    zero_range(frame, L.off[0] + n, L.off[1]);
+    zero_range(frame, L.off[1] + pb, L.off[2]);
+    zero_range(frame, L.off[2] + pb, L.off[3]);
+    zero_range(frame, L.off[3] + pb, L.off[4]);
+    zero_range(frame, L.off[4] + 4 * L.groups, L.off[5]);
+    zero_range(frame, L.off[5] + zc, L.off[5] + pad128(zc));
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+struct SmallDecShared {
+  HeaderInfo h;
+  int32_t err;
+};
+
+__global__ void __launch_bounds__(kSmallThreads)
+decode_small_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_t* __restrict__ err,
+                    int write_out, int pull) {
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ SmallDecShared S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rank = (int)cluster.block_rank(), C = (int)cluster.num_blocks();
+  const int seg = (int)(blockIdx.x / (unsigned)C);
+  if (tid == 0) {
+    bool ready = true;
+    if (pull && segs.ready[seg]) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_sys_u64(segs.ready[seg]) < segs.epoch) {
+        if (segs.timeout_ns > 0 && (int64_t)(globaltimer_ns() - t0) > segs.timeout_ns) {
+          ready = false;
+          break;
+        }
+        __nanosleep(128);
+      }
+    }
+    if (ready) {
+      S.h = check_header(segs.stat[seg], segs.n[seg], segs.dyn_len[seg]);
+      if (S.h.err == kOk && S.h.gsl != 9) S.h.err = kErrGroupSize;
+    } else {
+      S.h.err = kErrTimeout;
+    }
+    S.err = S.h.err == kOk ? 0x7F7F7F7F : S.h.err;   // atomicMin target: "ok" is largest
+  }
+  __syncthreads();
+  if (S.h.err == kOk) {
+    const HeaderInfo H = S.h;
+    const int64_t n = H.n;
+    const Layout L = layout_of(n, 9);
+    const uint8_t* frame = segs.stat[seg];
+    const uint8_t* dyn = segs.dyn[seg] ? segs.dyn[seg] : frame + L.off[5];
+    const uint32_t* gi = reinterpret_cast<const uint32_t*>(frame + L.off[4]);
+    uint16_t* o = out + segs.out_off[seg];
+    int32_t my_err = kOk;
+    const int64_t groups = L.groups;
+    for (int64_t g = (int64_t)rank * (kSmallThreads / 32) + warp; g < groups;
+         g += (int64_t)C * (kSmallThreads / 32)) {
+      const int64_t e0 = g * 512 + lane * 16;
+      const int64_t nv64 = n - e0;
+      const int nv = nv64 >= 16 ? 16 : (nv64 > 0 ? (int)nv64 : 0);
+      uint32_t S4[4] = {0, 0, 0, 0}, p0 = 0, p1 = 0, p2 = 0;
+      if (nv == 16) {
+        const uint4 s = ld_stream_v4(frame + L.off[0] + e0);
+        S4[0] = s.x; S4[1] = s.y; S4[2] = s.z; S4[3] = s.w;
+        const int64_t pb = e0 >> 3;
+        p0 = *reinterpret_cast<const uint16_t*>(frame + L.off[1] + pb);
+        p1 = *reinterpret_cast<const uint16_t*>(frame + L.off[2] + pb);
+        p2 = *reinterpret_cast<const uint16_t*>(frame + L.off[3] + pb);
+      } else if (nv > 0) {
+        for (int k = 0; k < nv; ++k) S4[k >> 2] |= (uint32_t)frame[L.off[0] + e0 + k] << (8 * (k & 3));
+        const int64_t pb = e0 >> 3;
+        p0 = frame[L.off[1] + pb]; p1 = frame[L.off[2] + pb]; p2 = frame[L.off[3] + pb];
+        if (nv > 8) {
+          p0 |= (uint32_t)frame[L.off[1] + pb + 1] << 8;
+          p1 |= (uint32_t)frame[L.off[2] + pb + 1] << 8;
+          p2 |= (uint32_t)frame[L.off[3] + pb + 1] << 8;
+        }
+      }
+      const uint32_t valid = nv >= 16 ? 0xFFFFu : (nv > 0 ? (1u << nv) - 1u : 0u);
+      const uint32_t escm = ~(p0 | p1 | p2) & valid;
+      const uint32_t c = __popc(escm);
+      const uint32_t incl = warp_incl_scan(c);
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      uint32_t gv = 0, gn = 0;
+      if (lane == 0) {
+        gv = gi[g];
+        gn = (g + 1 < groups) ? gi[g + 1] : (uint32_t)H.zc;
+        if (g == 0 && gv != 0) my_err = kErrGroupIndex;
+        if (gv + tot != gn) my_err = (g + 1 < groups) ? kErrGroupIndex : kErrZeroCount;
+      }
+      gv = __shfl_sync(0xffffffffu, gv, 0);
+      int64_t r = (int64_t)gv + (incl - c);
+      uint32_t ow[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t code = ((p0 >> j) & 1u) | ((p1 >> j) & 1u) << 1 | ((p2 >> j) & 1u) << 2;
+        uint32_t ex;
+        if (code) {
+          ex = prmt(H.tbl_lo, H.tbl_hi, code) & 0xFFu;
+        } else {
+          const int64_t q = r < H.zc ? r : (H.zc ? H.zc - 1 : 0);   // clamp: memory-safe
+          ex = (j < nv && H.zc) ? dyn[q] : 0u;
+          r += (j < nv) ? 1 : 0;
+        }
+        const uint32_t smb = (S4[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+        ow[j >> 1] |= ((smb & 0x80u) << 8 | ex << 7 | (smb & 0x7Fu)) << (16 * (j & 1));
+      }
+      if (write_out && nv > 0) {
+        uint16_t* d = o + e0;
+        if (nv == 16 && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+          st_stream_v4(d, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+          st_stream_v4(d + 8, make_uint4(ow[4], ow[5], ow[6], ow[7]));
+        } else {
+          for (int j = 0; j < nv; ++j) d[j] = (uint16_t)(ow[j >> 1] >> (16 * (j & 1)));
+        }
+      }
+    }
+    if (lane == 0 && my_err != kOk) atomicMin(&S.err, my_err);
+  }
+  cluster.sync();                                           // every CTA's error posted
+  if (rank == 0 && tid == 0) {
+    int32_t e = S.err;
+    for (int r = 1; r < C; ++r) {
+      const int32_t v = *cluster.map_shared_rank(&S.err, r);
+      if (v < e) e = v;
+    }
+    err[seg] = e;
+  }
+  cluster.sync();                                           // DSMEM reads done
+}
+
+// ---------------------------------------------------------------------------
+
+static int small_ctas_for(int64_t n) {
+  int64_t c = (n + kTile - 1) / kTile;                     // >= one tile per CTA
+  if (c > kSmallCtas) c = kSmallCtas;
+  if (c < 1) c = 1;
+  return (int)c;
+}
+
+// Measured crossover (scripts/exp/small_parts.py, graph replay): the one-launch
+// encoder wins up to 256 KiB (12.4 vs 16.2 us codebook + encode), the
+// two-pass encoder with 148 SMs from 512 KiB on (16.4 vs 18.7 us).
+bool small_encode_ok(int64_t n, int gsl) {
+  static const int64_t lim = [] {
+    const char* e = getenv("ZC_SMALL_MAX_WORDS");
+    return e ? (int64_t)atoll(e) : (int64_t)131072;
+  }();
+  return gsl == 9 && n >= 1 && n <= lim && n <= kSmallMaxWords;
+}
+
+cudaError_t launch_encode_small(const uint16_t* x, int64_t n, const uint8_t* book_in,
+                                uint8_t* frame, uint64_t* frame_len, uint8_t* book_out,
+                                double* result, cudaStream_t st) {
+  const int C0 = small_ctas_for(n);
+  int64_t wpc = (n + C0 - 1) / C0;
+  wpc = (wpc + 511) / 512 * 512;
+  const int C = (int)((n + wpc - 1) / wpc);
+  const size_t dyn = (size_t)(2 * wpc) + (size_t)(wpc / 512) * 32 * 2;
+  static int set[kMaxDevices];
+  per_device(set, [] {
+    cudaFuncSetAttribute(encode_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * kSmallCtaWords + (kSmallCtaWords / 512) * 64));
+    return 1;
+  });
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)C);
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, encode_small_kernel, x, n, wpc, book_in, frame, frame_len,
+                            book_out, result);
+}
+
+// flags: bit 0 write the words, bit 2 pull (wait for each segment's ready flag)
+cudaError_t launch_decode_small(const DecodeSegs& segs, uint16_t* out, int32_t* err, int flags,
+                                cudaStream_t st) {
+  int64_t nmax = 0;
+  for (int s = 0; s < segs.nseg; ++s) nmax = segs.n[s] > nmax ? segs.n[s] : nmax;
+  const int C = small_ctas_for(nmax);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(C * segs.nseg));
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_small_kernel, segs, out, err, flags & 1,
+                            (flags >> 2) & 1);
+}
+
+cudaError_t preload_small() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, (const void*)encode_small_kernel);
+  cudaFuncGetAttributes(&a, (const void*)decode_small_kernel);
+  return cudaGetLastError();
+}
+
+}  // namespace zc

@@ -184,24 +184,7 @@ __device__ void finalize_block(const Partial* parts, int64_t nparts, int64_t tot
       chan_merge(cn, cm, cq, f_n[i], f_m[i], f_q[i]);
       if (ce < 0) ce = f_e[i];
     }
-    const double sigma = cn > 0.0 ? sqrt(cq / cn) : nan("");
-    result[0] = sigma;
-    result[1] = cn;
-    if (cn > 0.0 && isfinite(sigma) && sigma > 0.0) {
-      write_window(book, derive_base(sigma));
-      result[2] = 1.0;
-    } else {
-      // modal fallback (codec.py:181-185): with sigma 0 or no finite value the
-      // histogram has at most two bins, the common finite exponent and 255
-      const double c_nf = (double)total_words - cn;
-      int mode;
-      if (cn > 0.0 && cn >= c_nf) mode = ce;
-      else if (total_words > 0) mode = 255;
-      else mode = 0;
-      const bool all_zero_exp = (mode == 0) && (cn == (double)total_words);
-      write_window(book, all_zero_exp ? -6 : mode - 127 - 3);
-      result[2] = 2.0;
-    }
+    finish_codebook(cn, cq, ce, total_words, book, result);
   }
 }
 

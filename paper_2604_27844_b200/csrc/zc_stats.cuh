@@ -244,6 +244,31 @@ __device__ inline void write_window(uint8_t* book, int base) {
 }
 
 
+// The reference derivation from merged statistics (count cn, M2 cq, first
+// finite exponent ce): result[0] = sigma (NaN when no finite value),
+// result[1] = finite count, result[2] = path (1 analytic, 2 modal).
+__device__ inline void finish_codebook(double cn, double cq, int ce, int64_t total_words,
+                                       uint8_t* book, double* result) {
+  const double sigma = cn > 0.0 ? sqrt(cq / cn) : nan("");
+  result[0] = sigma;
+  result[1] = cn;
+  if (cn > 0.0 && isfinite(sigma) && sigma > 0.0) {
+    write_window(book, derive_base(sigma));
+    result[2] = 1.0;
+  } else {
+    // modal fallback (codec.py:181-185): with sigma 0 or no finite value the
+    // histogram has at most two bins, the common finite exponent and 255
+    const double c_nf = (double)total_words - cn;
+    int mode;
+    if (cn > 0.0 && cn >= c_nf) mode = ce;
+    else if (total_words > 0) mode = 255;
+    else mode = 0;
+    const bool all_zero_exp = (mode == 0) && (cn == (double)total_words);
+    write_window(book, all_zero_exp ? -6 : mode - 127 - 3);
+    result[2] = 2.0;
+  }
+}
+
 // ---- certified fast statistic ------------------------------------------------
 // Every element contributes d = x - K (K = the first element when finite, else
 // 0; the same K everywhere, so partials merge by plain addition) to per-tile

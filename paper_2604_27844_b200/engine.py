@@ -204,15 +204,18 @@ def encode_measured(words: torch.Tensor, segs, gs_log2: int, frames: torch.Tenso
 
 def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_offs,
            write_out: bool = True, err: torch.Tensor | None = None, stream=None,
-           device=None, large_groups: bool = False) -> torch.Tensor:
+           device=None, large_groups: bool = False, groups512: bool = False) -> torch.Tensor:
     """K3/K5: decode (and validate) one frame per segment.
 
     stat_ptrs/dyn_ptrs are raw device addresses (local or peer-mapped);
     dyn_ptrs entries may be 0 for "dynamic section in place".  Returns the
     int32[nseg] device error words (0x7F7F7F7F = ok).  ``large_groups``
-    must be set when a frame may use groups larger than 4096 elements.
+    must be set when a frame may use groups larger than 4096 elements;
+    ``groups512`` asserts the default 512-element groups (frames of the
+    collectives and of compress(..., 512)), which lets messages of up to
+    512 Ki words take the one-launch cluster decoder.
     """
-    flags = (1 if write_out else 0) | (2 if large_groups else 0)
+    flags = (1 if write_out else 0) | (2 if large_groups else 0) | (8 if groups512 else 0)
     nseg = len(counts)
     dev = out.device if out is not None else torch.device(device or "cuda")
     if err is None:

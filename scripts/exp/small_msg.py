@@ -20,7 +20,7 @@ for kib in [int(a) for a in sys.argv[1:]] or [64, 256, 2048]:
 
     def step():
         engine.encode_measured(w, [(0, n)], 9, frames, [0], flen)
-        engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err)
+        engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err, groups512=True)
     step()
     torch.cuda.synchronize()
     assert torch.equal(out, w)

@@ -42,7 +42,7 @@ for kib in [int(a) for a in sys.argv[1:]] or [64, 256, 1024, 2048]:
     enc = lambda: engine.encode_measured(w, [(0, n)], 9, frames, [0], flen)  # noqa: E731
     enc_only = lambda: engine.encode(w, [(0, n)], book, 9, frames, [0], flen)  # noqa: E731
     stats = lambda: engine.measured_codebook(w)  # noqa: E731
-    dec = lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err)  # noqa: E731
+    dec = lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err, groups512=True)  # noqa: E731
     both = lambda: (enc(), dec())  # noqa: E731
     enc()
     dec()

@@ -468,3 +468,45 @@ def test_zbf16_round_trip(tmp_path):
     assert path.read_bytes() == zo.encode(data, zc.derive_codebook(1.0).entries)
     back = zc.decompress(container.read_zbf16(path))
     assert np.array_equal(back.cpu().numpy().view(np.uint16), data)
+
+
+@pytest.mark.parametrize("n", [1, 15, 511, 512, 513, 4095, 4096, 4097, 12_345, 65_536,
+                               131_071, 131_072, 131_073])
+@pytest.mark.parametrize("shift", [0, 1, 8])
+def test_small_message_path_matches_oracle(n, shift):
+    """One-launch cluster encoder / decoder (zc_small.cu) at the sizes around
+    its CTA split and its threshold, with 16-B aligned (TMA) and misaligned
+    inputs, specials included; frames byte-identical to the oracle."""
+    words = zo.gaussian(n + shift, 0.02, seed=n % 97)
+    if n >= 8:
+        words[shift:shift + 6] = [0x7FC0, 0x7F80, 0xFF80, 0x0000, 0x8000, 0x0001]
+    base = torch.from_numpy(words.view(np.int16)).cuda()
+    x = base[shift:]
+    book = zc.codebook_for(x)
+    want_book = zo.book_for(words[shift:])
+    assert book.entries == want_book
+    frame = zc.serialize(zc.compress(x, book))
+    assert frame == zo.encode(words[shift:], want_book)
+    # fused codebook_for + compress (the measured one-launch path)
+    f2 = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    b2, res, flen = engine.encode_measured(x, [(0, n)], 9, f2, [0])
+    assert tuple(b2[:7].cpu().tolist()) == want_book
+    assert bytes(f2[:int(flen.item())].cpu().numpy()) == frame
+    out = torch.empty(n + 3, dtype=torch.int16, device="cuda")[3:]      # misaligned output
+    err = engine.decode([f2.data_ptr()], [0], None, [n], out, [0], groups512=True)
+    assert int(err[0].item()) == engine.ERR_OK and torch.equal(out, x)
+
+
+def test_small_decoder_rejects_foreign_group_size_and_corruption():
+    words = zo.gaussian(3000, 1.0, seed=5)
+    x = torch.from_numpy(words.view(np.int16)).cuda()
+    chunk = zc.compress(x, zc.codebook_for(x), group_size=256)
+    out = torch.empty_like(x)
+    err = engine.decode([chunk.frame.data_ptr()], [0], None, [3000], out, [0], groups512=True)
+    assert int(err[0].item()) == 22                   # the caller's 512 promise was wrong
+    assert torch.equal(zc.decompress(chunk), x)      # the general decoder handles it
+    f = zc.compress(x, zc.codebook_for(x)).frame.clone()
+    off_gi = codec.section_offsets(3000, 512)[4]
+    f[off_gi + 4] ^= 1                                 # group_index[1] off by one
+    err = engine.decode([f.data_ptr()], [0], None, [3000], out, [0], groups512=True)
+    assert int(err[0].item()) == 17                    # "group_index" (reference field)
