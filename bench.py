@@ -861,6 +861,73 @@ def run_moe_a2a(args):
     dist.destroy_process_group()
 
 
+def run_imbalance(args):
+    """SURVEY §8(f)4 / PAPER.md:301-311, :433: design 2 absorbing start skew.
+    Every step, rank 1 starts its all-to-all `--skew-us` late (a device-side
+    sleep on its stream, like a slow expert computation); the metric is the
+    slowest rank's time from the common start to the end of the collective,
+    for design 1 and design 2 on the message plane and for the peer-memory
+    plane, against the same skew on the plain NCCL all-to-all.  Needs >= 2
+    GPUs (thread ranks sharing one GPU would serialise the skew)."""
+    import torch
+    import torch.distributed as dist
+    world, rank, local, dev = _init_dist(args)
+    from paper_2604_27844_b200 import collectives as coll
+    comm = setup_comm(args, dev)
+    hidden, rows = 4096, args.tokens * 8 // world
+    g = torch.Generator(device=dev).manual_seed(7 + rank)
+    x = torch.randn(world * rows * hidden, device=dev, generator=g).to(torch.bfloat16)
+    counts = [rows * hidden] * world
+    chunks = [x[q * rows * hidden:(q + 1) * rows * hidden] for q in range(world)]
+    spec = coll.AlltoAllSpec(chunks, counts)
+    out = torch.empty_like(x)
+    cycles = int(args.skew_us * 1e-6 * 1.9e9)
+    variants = {"raw_nccl": lambda: dist.all_to_all_single(out, x)}
+    if comm.bench_plane != "generic":
+        comm.native.reserve(int(1.05 * world * (2.4 * rows * hidden + 4096)))
+
+        def with_plane(plane, fn):
+            def run():
+                comm.native.plane = plane
+                return fn(comm, spec)
+            return run
+        variants["zip_d1_msg"] = with_plane("msg", coll.zip_all_to_all_d1)
+        variants["zip_d2_msg"] = with_plane("msg", coll.zip_all_to_all_d2)
+        if comm.bench_plane == "p2p":
+            variants["zip_p2p"] = with_plane("p2p", coll.zip_all_to_all_d2)
+    res = {}
+    for name, fn in variants.items():
+        for skew in (0, cycles):
+            for _ in range(args.warmup):
+                fn()
+            torch.cuda.synchronize()
+            times = []
+            for _ in range(args.steps):
+                dist.barrier()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                if rank == 1 and skew:
+                    torch.cuda._sleep(skew)
+                fn()
+                b.record()
+                torch.cuda.synchronize()
+                times.append(a.elapsed_time(b))
+            t = torch.tensor([sum(times) / len(times)], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            res[f"{name}{'_skewed' if skew else ''}_ms"] = float(t.item())
+    if comm.bench_plane != "generic":
+        comm.native.plane = comm.bench_plane
+    if rank == 0:
+        for name in variants:
+            res[f"{name}_skew_cost_ms"] = res[f"{name}_skewed_ms"] - res[f"{name}_ms"]
+        print(json.dumps({"metric": METRIC, "workload": "imbalance study: all-to-all under "
+                          f"{args.skew_us} us start skew on rank 1", "n_gpus": world,
+                          "rows_per_peer": rows, "hidden": hidden, "unit": "ms",
+                          "results": res, "plane": comm.bench_plane}), flush=True)
+    dist.destroy_process_group()
+
+
 def run_sweep(args):
     """BASELINE configs[4]: message sizes 64 KiB .. 1 GiB (per rank).
 
@@ -1001,12 +1068,13 @@ def main():
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the N=1 step eagerly (default: CUDA graph replays)")
     ap.add_argument("--workload", default="layer_ag",
-                    choices=["layer_ag", "moe_a2a", "grad_mix", "sweep"],
+                    choices=["layer_ag", "moe_a2a", "grad_mix", "sweep", "imbalance"],
                     help="layer_ag: the headline line (configs[1]); moe_a2a: configs[2]; "
                          "grad_mix: configs[3]; sweep: configs[4]")
     ap.add_argument("--tokens", type=int, default=4096, help="moe_a2a tokens per rank")
     ap.add_argument("--routing", default="uniform", choices=["uniform", "zipf"],
                     help="moe_a2a expert routing")
+    ap.add_argument("--skew-us", type=float, default=200.0, help="imbalance: rank 1 start delay")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
                     help="nccl: the message plane (reference protocols over NCCL); "
@@ -1026,6 +1094,8 @@ def main():
         run_moe_a2a(args)
     elif args.workload == "sweep":
         run_sweep(args)
+    elif args.workload == "imbalance":
+        run_imbalance(args)
     else:
         run_ours(args)
 
