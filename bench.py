@@ -856,7 +856,7 @@ def run_moe_a2a(args):
             "raw_value": float(tot.item()) / (ms["raw"] / 1e3) / 1e9,
             "algbw_GBps": algbw, "busbw_GBps": algbw * (world - 1) / world,
             "speedup_zip_over_raw": ms["raw"] / ms["zip"], "plane": comm.bench_plane,
-            "raw": "torch.distributed.all_to_all_single (NCCL), same splits",
+            "raw": f"torch.distributed.all_to_all_single ({args.backend}), same splits",
             "nccl": nccl_info(), "backend": args.backend}), flush=True)
     dist.destroy_process_group()
 

@@ -41,6 +41,7 @@ class _Workspace:
 
     def __init__(self, buf, lock):
         self.buf, self.lock = buf, lock
+        self._guard = None
 
     def data_ptr(self):
         return self.buf.data_ptr()
@@ -50,9 +51,14 @@ class _Workspace:
 
     def __enter__(self):
         self.lock.acquire()
+        # launches inside go to the tensors' device and its current stream,
+        # whatever device is current in the calling thread
+        self._guard = torch.cuda.device(self.buf.device)
+        self._guard.__enter__()
         return self
 
     def __exit__(self, *exc):
+        self._guard.__exit__(*exc)
         self.lock.release()
 
 
@@ -242,8 +248,9 @@ def decode_groups(frame: torch.Tensor, n: int, gs_log2: int, g0: int, g1: int,
     if out is None:
         out = torch.empty(count, dtype=torch.int16, device=frame.device)
     if count:
-        check(lib().zc_decode_groups(frame.data_ptr(), int(n), int(gs_log2), int(g0), int(g1),
-                                     out.data_ptr(), stream_ptr(stream)), "zc_decode_groups")
+        with torch.cuda.device(frame.device):
+            check(lib().zc_decode_groups(frame.data_ptr(), int(n), int(gs_log2), int(g0), int(g1),
+                                         out.data_ptr(), stream_ptr(stream)), "zc_decode_groups")
     return out
 
 

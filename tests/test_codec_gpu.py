@@ -510,3 +510,22 @@ def test_small_decoder_rejects_foreign_group_size_and_corruption():
     f[off_gi + 4] ^= 1                                 # group_index[1] off by one
     err = engine.decode([f.data_ptr()], [0], None, [3000], out, [0], groups512=True)
     assert int(err[0].item()) == 17                    # "group_index" (reference field)
+
+
+def test_decompress_out_is_validated():
+    # a short / non-contiguous / foreign-device `out` must not be
+    # written past its end or silently replaced by a copy
+    words = zo.gaussian(5000, 0.02, seed=3)
+    x = torch.from_numpy(words.view(np.int16)).cuda()
+    chunk = zc.compress(x, zc.codebook_for(x))
+    with pytest.raises(ValueError):
+        zc.decompress(chunk, out=torch.empty(4999, dtype=torch.int16, device="cuda"))
+    with pytest.raises(ValueError):
+        zc.decompress(chunk, out=torch.empty(10000, dtype=torch.int16, device="cuda")[::2])
+    with pytest.raises(ValueError):
+        zc.decompress(chunk, out=torch.empty(5000, dtype=torch.int16))
+    with pytest.raises(ValueError):
+        zc.decompress(chunk, out=torch.empty(5000, dtype=torch.int32, device="cuda"))
+    out = torch.empty(5000, dtype=torch.bfloat16, device="cuda")
+    zc.decompress(chunk, out=out)
+    assert torch.equal(out.view(torch.int16), x)
