@@ -163,9 +163,12 @@ def setup_comm(args, dev):
             else:
                 comm.use_native = True
                 native = comm.native
-                if plane == "p2p" and not native.p2p_available:
+                if native is None:                    # gloo group: no native engine
                     ok = 0
-                native.plane = plane
+                elif plane == "p2p" and not native.p2p_available:
+                    ok = 0
+                else:
+                    native.plane = plane
             if ok:
                 got = coll.zip_all_gather(comm, x)
                 ok = int(torch.equal(got.view(torch.int16), ref.view(torch.int16)))
@@ -895,6 +898,9 @@ def run_imbalance(args):
         variants["zip_d2_msg"] = with_plane("msg", coll.zip_all_to_all_d2)
         if comm.bench_plane == "p2p":
             variants["zip_p2p"] = with_plane("p2p", coll.zip_all_to_all_d2)
+    else:                                  # the Python protocols over the group's byte movers
+        variants["zip_d1_generic"] = lambda: coll.zip_all_to_all_d1(comm, spec)
+        variants["zip_d2_generic"] = lambda: coll.zip_all_to_all_d2(comm, spec)
     res = {}
     for name, fn in variants.items():
         for skew in (0, cycles):

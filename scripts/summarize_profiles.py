@@ -64,6 +64,14 @@ def kernel_summary(tag, kname):
              and d[k] not in ("", "n/a")}
     lines.append("pipes (% of peak, active): " + ", ".join(
         f"{k}={v:.0f}" for k, v in sorted(pipes.items(), key=lambda x: -x[1])[:8]))
+    st = {k[len("smsp__pcsamp_warps_issue_stalled_"):]: float(d[k]) for k in d
+          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")
+          and d[k] not in ("", "n/a")}
+    stot = sum(st.values()) or 1.0
+    lines.append("stall reasons (% of samples): " + ", ".join(
+        f"{k}={100 * v / stot:.1f}" for k, v in sorted(st.items(), key=lambda x: -x[1])[:9]))
+    if "smsp__warps_eligible.avg.per_cycle_active" in d:
+        lines.append(f"warps eligible per cycle = {d['smsp__warps_eligible.avg.per_cycle_active']}")
     out = subprocess.run(["ncu", "-i", str(rep), "--page", "source", "--csv"], capture_output=True,
                          text=True).stdout
     r = csv.reader(out.splitlines())
