@@ -17,6 +17,8 @@
 //   elements accumulate into one register whose bytes are plane0/1/2/escape
 //   group_index / escapes placed by the look-back prefix.
 // Bytes per element: 2 read + ~1.40 written (HBM bound, no tensor cores).
+#include <type_traits>
+
 #include "zc_stats.cuh"
 
 namespace zc {
@@ -506,10 +508,16 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
               (prmt(b.x, b.y, 0x7531) << 1 & 0xFEFEFEFEu) | (prmt(b.x, b.y, 0x6420) >> 7 & 0x01010101u),
               (prmt(b.z, b.w, 0x7531) << 1 & 0xFEFEFEFEu) | (prmt(b.z, b.w, 0x6420) >> 7 & 0x01010101u)};
           __syncthreads();
+          // the staged run starts at the same address mod 16 as its scratch
+          // destination, so the copy-out below is 16-B words on both sides
+          // (bytes only at the ends, which neighbouring warps' runs share)
+          uint8_t* dst = esc_out + (lp - excl);          // the warp's first escape
+          const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 15u);
+          const uint32_t s0 = smem_u32(sb) + mis;        // staged byte i <-> dst[i]
           // shared accesses as asm without a memory clobber: ordered by the
           // block barriers around them, invisible to the compiler's alias
           // analysis of the hot loop (plain C++ stores here cost it 2 us)
-          uint32_t p = smem_u32(sb) + excl;
+          uint32_t p = s0 + excl;
 #pragma unroll
           for (int j = 0; j < kEPT; ++j)
             if (esc & (1u << j)) {
@@ -517,11 +525,23 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
               ++p;
             }
           __syncthreads();
-          uint8_t* dst = esc_out + (lp - excl);          // the warp's first escape
-          const uint32_t sb32 = smem_u32(sb);
-          for (uint32_t i = lane; i < wtot; i += 32) {
+          const uint32_t h16 = (16u - mis) & 15u;
+          const uint32_t head = wtot < h16 ? wtot : h16;
+          const uint32_t nbody = (wtot - head) >> 4;
+          if (lane < head) {
             uint32_t v;
-            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sb32 + i));
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(s0 + lane));
+            dst[lane] = (uint8_t)v;
+          }
+          for (uint32_t i = lane; i < nbody; i += 32) {
+            uint4 v;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(s0 + head + 16u * i));
+            *reinterpret_cast<uint4*>(dst + head + 16u * i) = v;
+          }
+          for (uint32_t i = head + 16u * nbody + lane; i < wtot; i += 32) {
+            uint32_t v;
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(s0 + i));
             dst[i] = (uint8_t)v;
           }
         };
@@ -789,16 +809,38 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
         if (j < lim) dst[b0 + j] = (uint8_t)(wv[j >> 2] >> (8 * (j & 3)));
     }
   } else {
-    const uint32_t head = (uint32_t)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
-    const uint32_t h = run < head ? run : head;
-    if (tid < h) dst[tid] = esc_out[tid];
-    const uint32_t body = (run - h) / 4;
-    uint32_t* dst4 = reinterpret_cast<uint32_t*>(dst + h);
-    for (uint32_t i = tid; i < body; i += kThreads) {
-      const uint8_t* q = esc_out + h + 4 * i;
-      dst4[i] = (uint32_t)q[0] | (uint32_t)q[1] << 8 | (uint32_t)q[2] << 16 | (uint32_t)q[3] << 24;
+    // escape-heavy run: 16-B aligned stores built by funnel shifts from two
+    // 16-B aligned scratch loads (the scratch run starts 16-B aligned, its
+    // frame position at any byte)
+    const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 15u);
+    const uint32_t h16 = (16u - mis) & 15u;
+    const uint32_t head = run < h16 ? run : h16;
+    if (tid < head) dst[tid] = esc_out[tid];
+    const uint32_t nbody = (run - head) >> 4;
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    const uint4* s4 = reinterpret_cast<const uint4*>(esc_out);
+    const uint32_t sh = 8u * (head & 3u);
+    // body word i = scratch bytes [head + 16 i, head + 16 i + 16): words
+    // q .. q + 4 of the pair (s4[i], s4[i + 1]), q = head / 4
+    auto body = [&](auto qc) {
+      constexpr int q = decltype(qc)::value;
+      for (uint32_t i = tid; i < nbody; i += kThreads) {
+        const uint4 a = __ldcs(s4 + i);
+        const uint4 b = head ? __ldcs(s4 + i + 1) : a;   // starts inside the run when head > 0
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        __stcs(d4 + i, make_uint4(__funnelshift_r(w[q], w[q + 1], sh),
+                                  __funnelshift_r(w[q + 1], w[q + 2], sh),
+                                  __funnelshift_r(w[q + 2], w[q + 3], sh),
+                                  __funnelshift_r(w[q + 3], w[q + 4], sh)));
+      }
+    };
+    switch (head >> 2) {
+      case 0: body(std::integral_constant<int, 0>{}); break;
+      case 1: body(std::integral_constant<int, 1>{}); break;
+      case 2: body(std::integral_constant<int, 2>{}); break;
+      default: body(std::integral_constant<int, 3>{}); break;
     }
-    for (uint32_t i = h + 4 * body + tid; i < run; i += kThreads) dst[i] = esc_out[i];
+    for (uint32_t i = head + 16u * nbody + tid; i < run; i += kThreads) dst[i] = esc_out[i];
   }
   if ((int)blockIdx.x == rp.run_start[seg + 1] - 1) {
     const uint64_t zc = P + run;
