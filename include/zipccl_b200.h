@@ -132,6 +132,21 @@ int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64
               const int64_t* n, const int64_t* out_off, int nseg, uint16_t* out,
               int32_t* err_dev, void* ws, int64_t ws_bytes, int write_out, void* stream);
 
+/* Decode behind arrival: the per-peer decode of the reference's receive
+ * loop (collectives.py:216-227) as ONE launch over frames that are still
+ * arriving.  Frame s (its static part at stat[s], 16-B aligned, the dynamic
+ * section in place) is decoded once *ready[s] >= epoch (acquire load at
+ * system scope; the writer publishes after its frame with a release store or
+ * a completed copy), in whatever order the flags appear: work on the frames
+ * already complete proceeds while later ones are in flight.  Frames of n[s]
+ * elements with groups of <= 4096 elements; words to out + out_off[s].
+ * err_dev[s] as zc_decode; 20 if the flag did not arrive within timeout_ns
+ * (0: wait forever).  ws >= zc_workspace_bytes(sum n, nseg). */
+int zc_decode_when_ready(const uint8_t* const* stat, const int64_t* n, const int64_t* out_off,
+                         const uint64_t* const* ready, int nseg, uint64_t epoch,
+                         int64_t timeout_ns, uint16_t* out, int32_t* err_dev, void* ws,
+                         int64_t ws_bytes, void* stream);
+
 /* Replaces codec.decompress_group (codec.py:330-348), generalised to a
  * range: the words of groups [g0, g1) of a frame of n elements with group
  * size 1 << gs_log2 are written to out[0 ..), reading only those groups'

@@ -48,6 +48,8 @@ EXPORTS = {
     "zc_decode": (_int, [_P(_vp), _P(_vp), _P(_i64), _P(_i64), _P(_i64), _int, _vp, _vp, _vp,
                          _i64, _int, _vp]),
     "zc_decode_groups": (_int, [_vp, _i64, _int, _i64, _i64, _vp, _vp]),
+    "zc_decode_when_ready": (_int, [_P(_vp), _P(_i64), _P(_i64), _P(_vp), _int, ctypes.c_uint64,
+                                    _i64, _vp, _vp, _vp, _i64, _vp]),
     "zc_ipc_handle_bytes": (_int, []),
     "zc_ipc_get_handle": (_int, [_vp, _vp]),
     "zc_ipc_open_handle": (_int, [_vp, _P(_vp)]),

@@ -257,6 +257,33 @@ int zc_decode(const uint8_t* const* stat, const uint8_t* const* dyn, const int64
   return status_of(launch_decode(s, out, err_dev, ws, write_out & 11, stream));
 }
 
+int zc_decode_when_ready(const uint8_t* const* stat, const int64_t* n, const int64_t* out_off,
+                         const uint64_t* const* ready, int nseg, uint64_t epoch,
+                         int64_t timeout_ns, uint16_t* out, int32_t* err_dev, void* ws,
+                         int64_t ws_bytes, cudaStream_t stream) {
+  Range nvtx_range("zc_decode_when_ready");
+  if (nseg < 1 || nseg > kMaxSegments || !stat || !n || !ready || !out || !err_dev || !ws)
+    return kStatusBadArg;
+  DecodeSegs s{};
+  s.nseg = nseg;
+  s.epoch = epoch;
+  s.timeout_ns = timeout_ns;
+  s.tile_start[0] = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (n[i] < 1 || !stat[i] || (reinterpret_cast<uintptr_t>(stat[i]) & 15) != 0) return kStatusBadArg;
+    s.stat[i] = stat[i];
+    s.dyn[i] = nullptr;
+    s.dyn_len[i] = -1;
+    s.n[i] = n[i];
+    s.out_off[i] = out_off ? out_off[i] : 0;
+    s.ready[i] = ready[i];
+    s.tile_start[i + 1] = s.tile_start[i] + tiles_of(n[i]);
+  }
+  if (128 + 8 * s.tile_start[nseg] + 256 > ws_bytes) return kStatusWorkspace;
+  // bit 0 write, bit 2 pull mode (the ring decoder; frames of <= 4096-element groups)
+  return status_of(launch_decode(s, out, err_dev, ws, 1 | 4, stream));
+}
+
 int zc_decode_groups(const uint8_t* frame, int64_t n, int gs_log2, int64_t g0, int64_t g1,
                      uint16_t* out, cudaStream_t stream) {
   Range nvtx_range("zc_decode_groups");

@@ -240,6 +240,25 @@ def decode(stat_ptrs, dyn_ptrs, dyn_lens, counts, out: torch.Tensor | None, out_
     return err
 
 
+def decode_when_ready(stat_ptrs, counts, out: torch.Tensor, out_offs, ready_ptrs, epoch: int,
+                      timeout_ns: int = 0, err: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """Decode frame s once the u64 at ready_ptrs[s] reaches ``epoch``, the
+    frames in the order their flags appear (zc_decode_when_ready; the
+    reference decodes each peer inside its receive loop, collectives.py:216-227).
+    Returns the int32[nseg] error words (20: flag timed out)."""
+    nseg = len(counts)
+    if err is None:
+        err = torch.empty(nseg, dtype=torch.int32, device=out.device)
+    total = sum(int(c) for c in counts)
+    with workspace(total, nseg, out.device, stream) as ws:
+        check(lib().zc_decode_when_ready(
+            ptrs(stat_ptrs), i64s(counts), i64s(out_offs), ptrs(ready_ptrs), nseg,
+            int(epoch), int(timeout_ns), out.data_ptr(), err.data_ptr(), ws.data_ptr(),
+            ws.numel(), stream_ptr(stream)), "zc_decode_when_ready")
+    return err
+
+
 def decode_groups(frame: torch.Tensor, n: int, gs_log2: int, g0: int, g1: int,
                   out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Words of groups [g0, g1) of a validated frame (zc_decode_groups)."""

@@ -529,3 +529,37 @@ def test_decompress_out_is_validated():
     out = torch.empty(5000, dtype=torch.bfloat16, device="cuda")
     zc.decompress(chunk, out=out)
     assert torch.equal(out.view(torch.int16), x)
+
+
+def test_decode_when_ready_decodes_late_frames_and_times_out():
+    # zc_decode_when_ready: frames decoded as their ready flags appear (the
+    # reference's per-peer decode inside its receive loop, collectives.py:216-227)
+    sizes = [4096 * 300 + 17, 70001, 4096 * 40]
+    xs = [engine.words_view((torch.randn(c, device="cuda") * 0.02).to(torch.bfloat16))
+          for c in sizes]
+    frames = [zc.compress(x, zc.codebook_for(x)).frame for x in xs]
+    out = torch.empty(sum(sizes), dtype=torch.int16, device="cuda")
+    offs = [0, sizes[0], sizes[0] + sizes[1]]
+    flags = torch.zeros(3, dtype=torch.int64, device="cuda")
+    ready = [flags.data_ptr() + 8 * i for i in range(3)]
+    flags[0] = 5
+    flags[2] = 5
+    side = torch.cuda.Stream()
+    err = engine.decode_when_ready([f.data_ptr() for f in frames], sizes, out, offs, ready, 5,
+                                   timeout_ns=10_000_000_000)
+    # the middle frame is published after the launch, from another stream
+    one = torch.full((1,), 5, dtype=torch.int64).pin_memory()
+    with torch.cuda.stream(side):   # a copy-engine write while the decode runs
+        flags[1:2].copy_(one, non_blocking=True)
+    torch.cuda.synchronize()
+    assert torch.all(err == engine.ERR_OK)
+    for x, o, c in zip(xs, offs, sizes):
+        assert torch.equal(out[o:o + c], x)
+    # a flag that never reaches the epoch: error word 20 (timeout) for that frame only
+    out.zero_()
+    flags[0] = 6
+    err = engine.decode_when_ready([f.data_ptr() for f in frames], sizes, out, offs, ready, 6,
+                                   timeout_ns=20_000_000)
+    codes = err.cpu().tolist()
+    assert codes[0] == engine.ERR_OK and codes[1] == 20 and codes[2] == 20
+    assert torch.equal(out[:sizes[0]], xs[0])
