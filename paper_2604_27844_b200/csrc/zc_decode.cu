@@ -506,38 +506,46 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
         const int64_t tb = t0 + lane;
         uint32_t bnd = 0;
         if (lane <= t1 - t0) bnd = tb < seg_tiles ? gi[tb * gpt] : (uint32_t)H.zc;
-        for (int64_t t = t0; t < t1; ++t) {
-          const int j = (int)(t - t0);
-          const int64_t lo = __shfl_sync(0xffffffffu, bnd, j);
-          const int64_t hi = __shfl_sync(0xffffffffu, bnd, j + 1);
-          if (lane == 0) {
-            const int st = (int)(k % kDStages);
-            if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
+        // lane j prepares tile t0 + j of the chunk (sizes, clamped escape
+        // range, group_index slice) in parallel; then the tiles are issued
+        // in order, tile j by lane j once its stage is free.  The lane-0
+        // serial path per tile is only the wait, the stage metadata and the
+        // bulk copies (~277 -> ~100 producer instructions per tile).
+        const int64_t t = t0 + lane;
+        const bool mine = t < t1;
+        const int64_t lo = (int64_t)bnd;
+        const int64_t hi = (int64_t)__shfl_down_sync(0xffffffffu, bnd, 1);
+        const int64_t e0 = t * kTile;
+        const int64_t valid = (n - e0) < kTile ? (n - e0) : kTile;
+        const uint32_t b_sm = mine ? r16(valid) : 0u, b_pl = mine ? r16((valid + 7) >> 3) : 0u;
+        // escapes: clamp into the section so a corrupt index stays memory-safe
+        const int64_t clo = lo < 0 ? 0 : (lo > H.zc ? H.zc : lo);
+        const int64_t chi = hi < clo ? clo : (hi > H.zc ? H.zc : hi);
+        const uint8_t* esrc = dyn + clo;
+        const uint8_t* eal = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(esrc) & ~uintptr_t(15));
+        int64_t eb = (int64_t)r16((uint64_t)(chi - clo) + (uint64_t)(esrc - eal));
+        if (eb > kEscSlots) eb = kEscSlots;
+        if ((eal - dyn) + eb > zcap + 128) eb = 0;   // never read past the padded section
+        // group_index slice [g0, g0 + ng] (+1 for the next tile's first entry)
+        uint32_t b_gi = 0;
+        const uint32_t* gsrc = gi;
+        int32_t shift = 0;
+        if (stage_gi && mine) {
+          const int64_t g0 = t * gpt;
+          int64_t ng = (valid + (int64_t(1) << gsl) - 1) >> gsl;
+          if (g0 + ng < L.groups) ng += 1;
+          const uint32_t* gp = gi + g0;
+          gsrc = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
+          shift = (int32_t)(gp - gsrc);
+          b_gi = r16((uint64_t)(ng + shift) * 4);
+        }
+        const int ntl = (int)(t1 - t0);
+        for (int jt = 0; jt < ntl; ++jt) {
+          if (lane == jt) {
+            const int64_t kk = k + jt;
+            const int st = (int)(kk % kDStages);
+            if (kk >= kDStages) mbar_wait(empty + st, (uint32_t)(((kk / kDStages) - 1) & 1));
             DStage& S = ring[st];
-            const int64_t e0 = t * kTile;
-            const int64_t valid = (n - e0) < kTile ? (n - e0) : kTile;
-            const uint32_t b_sm = r16(valid), b_pl = r16((valid + 7) >> 3);
-            // escapes: clamp into the section so a corrupt index stays memory-safe
-            int64_t clo = lo < 0 ? 0 : (lo > H.zc ? H.zc : lo);
-            int64_t chi = hi < clo ? clo : (hi > H.zc ? H.zc : hi);
-            const uint8_t* esrc = dyn + clo;
-            const uint8_t* eal = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(esrc) & ~uintptr_t(15));
-            int64_t eb = (int64_t)r16((uint64_t)(chi - clo) + (uint64_t)(esrc - eal));
-            if (eb > kEscSlots) eb = kEscSlots;
-            if ((eal - dyn) + eb > zcap + 128) eb = 0;   // never read past the padded section
-            // group_index slice [g0, g0 + ng] (+1 for the next tile's first entry)
-            uint32_t b_gi = 0;
-            const uint32_t* gsrc = gi;
-            int32_t shift = 0;
-            if (stage_gi) {
-              const int64_t g0 = t * gpt;
-              int64_t ng = (valid + (int64_t(1) << gsl) - 1) >> gsl;
-              if (g0 + ng < L.groups) ng += 1;
-              const uint32_t* gp = gi + g0;
-              gsrc = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
-              shift = (int32_t)(gp - gsrc);
-              b_gi = r16((uint64_t)(ng + shift) * 4);
-            }
             s_lo[st] = clo;
             s_al[st] = eal - dyn;
             s_cnt[st] = chi - clo;
@@ -552,8 +560,8 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
             if (eb) tma_load_1d(S.esc, eal, (uint32_t)eb, full + st);
           }
           __syncwarp();   // reconverge before the next shuffle (no BRA.DIV slow path)
-          ++k;
         }
+        k += ntl;
       }
       if (!kPull) c = (int64_t)__shfl_sync(0xffffffffu, nx, 0);
     }
