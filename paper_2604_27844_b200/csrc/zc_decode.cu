@@ -375,8 +375,12 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
   uint64_t* empty = full + kDStages;
   __shared__ __align__(16) uint32_t s_wsum[kDGroups][2][8];   // group x parity x virtual warp
   __shared__ HeaderInfo s_hdr[kMaxSegments];
-  __shared__ int64_t s_lo[kDStages], s_al[kDStages], s_cnt[kDStages], s_tile[kDStages];
-  __shared__ int32_t s_gi_shift[kDStages], s_seg[kDStages];
+  // per-stage metadata, one 16-B store / load: escape range start (lo),
+  // length, offset of lo in the staged escape bytes, and tile (24 bits) |
+  // segment (6) | group_index alignment shift (2); all ones = end marker
+  struct __align__(16) StageMeta { uint32_t lo, cnt; int32_t esc_off; uint32_t tsg; };
+  static_assert(kMaxSegments <= 64, "segment field");
+  __shared__ StageMeta s_meta[kDStages];
   __shared__ uint32_t s_spread[256];
   __shared__ __align__(16) uint8_t s_slot[kDGroups * 128 * 32];
   __shared__ uint32_t s_xsel[16];                    // expand selectors (expand_escapes)
@@ -546,12 +550,9 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
             const int st = (int)(kk % kDStages);
             if (kk >= kDStages) mbar_wait(empty + st, (uint32_t)(((kk / kDStages) - 1) & 1));
             DStage& S = ring[st];
-            s_lo[st] = clo;
-            s_al[st] = eal - dyn;
-            s_cnt[st] = chi - clo;
-            s_gi_shift[st] = shift;
-            s_tile[st] = t;
-            s_seg[st] = seg;
+            s_meta[st] = StageMeta{(uint32_t)clo, (uint32_t)(chi - clo),
+                                   (int32_t)(clo - (eal - dyn)),
+                                   (uint32_t)t | (uint32_t)seg << 24 | (uint32_t)shift << 30};
             mbar_arrive_expect_tx(full + st, b_sm + 3 * b_pl + b_gi + (uint32_t)eb);
             tma_load_1d(S.sm, frame + L.off[0] + e0, b_sm, full + st);
             for (int b = 0; b < 3; ++b)
@@ -569,7 +570,7 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
       for (int e = 0; e < kDGroups; ++e, ++k) {
         const int st = (int)(k % kDStages);
         if (k >= kDStages) mbar_wait(empty + st, (uint32_t)(((k / kDStages) - 1) & 1));
-        s_tile[st] = -1;
+        s_meta[st].tsg = 0xFFFFFFFFu;
         mbar_arrive(full + st);
       }
     }
@@ -604,9 +605,10 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
     const int64_t k = (int64_t)kDGroups * i + grp;
     const int st = (int)(k % kDStages);
     mbar_wait_warp(full + st, (uint32_t)((k / kDStages) & 1));
-    const int64_t t = s_tile[st];
-    if (t < 0) break;
-    const int seg = s_seg[st];
+    const StageMeta M = s_meta[st];
+    if (M.tsg == 0xFFFFFFFFu) break;
+    const int64_t t = M.tsg & 0xFFFFFFu;
+    const int seg = (int)((M.tsg >> 24) & 63u);
     if (seg != cseg) {                               // uniform across the group
       cseg = seg;
       const HeaderInfo& H = s_hdr[seg];
@@ -628,10 +630,10 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
     }
     const DStage& S = ring[st];
     const int64_t tile_base = t * kTile;
-    const int64_t lo = s_lo[st];
-    const int32_t tcnt = (int32_t)s_cnt[st];
-    const int32_t esc_off = (int32_t)(lo - s_al[st]);
-    const int gshift = s_gi_shift[st];
+    const int64_t lo = M.lo;
+    const int32_t tcnt = (int32_t)M.cnt;
+    const int32_t esc_off = M.esc_off;
+    const int gshift = (int)(M.tsg >> 30);
     const uint8_t* esc_base = S.esc + esc_off;   // this tile's staged escapes
     int32_t my_err = kOk;
     if (gs512 && tile_base + kTile <= n) {
