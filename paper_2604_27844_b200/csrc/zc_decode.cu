@@ -431,6 +431,11 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
         segs.nseg >= 64 ? ~0ull : ((1ull << segs.nseg) - 1ull);
     int cur = segs.nseg ? (int)(blockIdx.x % (unsigned)segs.nseg) : 0;
     const uint64_t t_begin = kPull ? globaltimer_ns() : 0;
+    // pull mode: the next chunk of the segment just selected is claimed
+    // right away and used on the next iteration, so the claim's round trip
+    // overlaps this chunk's issue (as the push path's one-ahead claim)
+    int pend_seg = -1;
+    unsigned pend = 0;
     if (!kPull && lane == 0) cl = atomicAdd(counter, 1u);
     int64_t c = (int64_t)__shfl_sync(0xffffffffu, cl, 0);
     while (true) {
@@ -440,6 +445,15 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
         int sel = -1, stop = 0;
         unsigned sel_c = 0;
         if (lane == 0) {
+          if (pend_seg >= 0) {
+            if ((int64_t)pend < cp.chunk_start[pend_seg + 1] - cp.chunk_start[pend_seg]) {
+              sel = pend_seg;
+              sel_c = pend;
+            } else {
+              seg_done |= 1ull << pend_seg;
+            }
+            pend_seg = -1;
+          }
           for (int i = 0; i < segs.nseg && sel < 0; ++i) {
             const int s2 = (cur + i) % segs.nseg;
             if ((seg_done >> s2) & 1ull) continue;
@@ -466,6 +480,10 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
             sel = s2;
             sel_c = cc;
             cur = s2;
+          }
+          if (sel >= 0) {
+            pend = atomicAdd(counter + 1 + sel, 1u);   // consumed next iteration
+            pend_seg = sel;
           }
           if (sel < 0) {
             if (seg_done == all_segs) {
