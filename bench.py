@@ -244,7 +244,46 @@ def cpu_baseline_sample(seconds: float = 10.0):
     assert np.array_equal(back, w)
     return {"value": 2 * n * reps / el / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{reps} x (codebook_for + encode + decode) of 2^24 N(0,0.02^2) BF16 "
-                      f"elements, numpy oracle port of the reference, {el:.1f} s"}
+                      f"elements, numpy oracle port of the reference, {el:.1f} s",
+            "c1_simulated_w2_allgather": c1_simulated_allgather()}
+
+
+def c1_simulated_allgather(world: int = 2, n: int = 1 << 23, trials: int = 3):
+    """BASELINE configs[0]'s second half: the reference's run_ranks(2,
+    zip_all_gather) timed like timed_call (transport.py:635-666,
+    collectives.py:366-376) -- thread ranks, each encodes its 2^23-element
+    shard, the frames are exchanged, every rank decodes its peers' frames and
+    concatenates in rank order; max over ranks, best of `trials`.  Run on the
+    numpy oracle port (same numpy primitives as the reference)."""
+    import threading
+    import numpy as np
+    from oracle import zc_oracle as zo
+    shards = [zo.rank_gaussian(r, n, s=0.02) for r in range(world)]
+    best = None
+    for _ in range(trials):
+        frames, outs, spans = [None] * world, [None] * world, [None] * world
+        bar = threading.Barrier(world)
+
+        def rank(r):
+            bar.wait()
+            t0 = time.perf_counter()
+            frames[r] = zo.encode(shards[r], zo.book_for(shards[r]))
+            bar.wait()                                   # the size + frame exchange
+            outs[r] = np.concatenate([shards[p] if p == r else zo.decode(frames[p])
+                                      for p in range(world)])
+            spans[r] = time.perf_counter() - t0
+        th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        want = np.concatenate(shards)
+        assert all(np.array_equal(o, want) for o in outs)
+        t = max(spans)
+        best = t if best is None else min(best, t)
+    return {"ms": 1e3 * best, "GBps": 2 * n * world / best / 1e9, "world": world,
+            "shard_elems": n, "threads": world,
+            "what": "run_ranks(2, zip_all_gather) on the oracle port: gathered bytes / max-over-ranks time"}
 
 
 def _oracle_worker(args):
