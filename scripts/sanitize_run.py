@@ -79,27 +79,52 @@ for _ in range(20):
     except (CorruptFrameError, CorruptChunkError):
         pass
 checks += 1
-# collectives on thread ranks sharing cuda:0: NCCL-style data plane (hub) and
-# the peer-memory pull-decode (signal / wait kernels, decoder on peer frames)
+# escape-heavy data (two-pass encoder: dense staging, the fix-up's shifted
+# 16-B copies of runs with > 4096 escapes), checked against the oracle
+from oracle import zc_oracle as zo  # noqa: E402
+n = 4096 * 1100 + 5
+v = torch.exp(torch.randn(n, device="cuda", generator=g) * 2.0 - 8.0)
+x = engine.words_view(v.to(torch.bfloat16))
+book = zc.codebook_for(x)
+fr = zc.serialize(zc.compress(x, book))
+assert fr == zo.encode(x.cpu().numpy().view(np.uint16), book.entries)
+assert torch.equal(zc.decompress(zc.parse(fr)), x)
+checks += 1
+# decode behind arrival (flags already set) and a timed-out flag
+x = words(4096 * 30 + 9)
+chunk = zc.compress(x, zc.codebook_for(x))
+flags = torch.tensor([3, 2], dtype=torch.int64, device="cuda")
+outd = torch.empty(2 * x.numel(), dtype=torch.int16, device="cuda")
+err = engine.decode_when_ready([chunk.frame.data_ptr()] * 2, [x.numel()] * 2, outd,
+                               [0, x.numel()], [flags.data_ptr(), flags.data_ptr() + 8], 3,
+                               timeout_ns=2_000_000)
+codes = err.cpu().tolist()
+assert codes[0] == engine.ERR_OK and codes[1] == 20 and torch.equal(outd[:x.numel()], x)
+checks += 1
+# collectives on native thread ranks sharing cuda:0: the message plane and
+# the peer-memory pull-decode, all-gather, all-to-all d1/d2, reduce-scatter
 from paper_2604_27844_b200 import collectives as coll  # noqa: E402
 from paper_2604_27844_b200.transport import run_ranks  # noqa: E402
 
 
 def body(comm):
     ok = True
-    for it in range(2):
-        local = words(200_003 + it)
-        ok &= torch.equal(coll.zip_all_gather(comm, local), coll.reference_all_gather(comm, local))
-        ok &= torch.equal(coll.zip_all_gather_p2p(comm, local),
-                          coll.reference_all_gather(comm, local))
-        sizes = [(comm.rank + d) * 3000 + 17 for d in range(comm.world_size)]
-        spec = coll.AlltoAllSpec([words(c) for c in sizes],
-                                 [(s + comm.rank) * 3000 + 17 for s in range(comm.world_size)])
-        z = coll.zip_all_to_all_p2p(comm, spec)
-        r = coll.reference_all_to_all(comm, spec)
-        ok &= all(torch.equal(a, b) for a, b in zip(z, r))
-        z = coll.zip_all_to_all_d2(comm, spec)
-        ok &= all(torch.equal(a, b) for a, b in zip(z, r))
+    for plane in ("msg", "p2p"):
+        comm.native.plane = plane
+        for it in range(2):
+            local = words(200_003 + it)
+            ok &= torch.equal(coll.zip_all_gather(comm, local),
+                              coll.reference_all_gather(comm, local))
+            sizes = [(comm.rank + d) * 3000 + 17 for d in range(comm.world_size)]
+            spec = coll.AlltoAllSpec([words(c) for c in sizes],
+                                     [(s + comm.rank) * 3000 + 17 for s in range(comm.world_size)])
+            r = coll.reference_all_to_all(comm, spec)
+            for fn in (coll.zip_all_to_all_d1, coll.zip_all_to_all_d2):
+                z = fn(comm, spec)
+                ok &= all(torch.equal(a, b) for a, b in zip(z, r))
+            xs = words(comm.world_size * 40_000)
+            ok &= torch.equal(coll.zip_reduce_scatter(comm, xs),
+                              coll.reference_reduce_scatter(comm, xs))
     return ok
 
 
