@@ -412,6 +412,9 @@ int t_sizes(zc_comm* c, const std::vector<uint64_t>& out_vals, int words_per_pee
   uint64_t* rbuf = sbuf + W * k;
   for (int i = 0; i < W * k; ++i) c->pinned[i] = out_vals[i];
   cudaMemcpyAsync(sbuf, c->pinned, sizeof(uint64_t) * W * k, cudaMemcpyHostToDevice, st);
+  // the self entries too, so the read-back below copies initialised memory only
+  cudaMemcpyAsync(rbuf + c->rank * k, sbuf + c->rank * k, sizeof(uint64_t) * k,
+                  cudaMemcpyDeviceToDevice, st);
   std::vector<Msg> s, r;
   for (int p = 0; p < W; ++p) {
     if (p == c->rank) continue;
@@ -874,7 +877,8 @@ int msg_a2a_exchange(zc_comm* c, const uint16_t* x, const int64_t* sc_, const in
   if (ce != cudaSuccess) return (int)ce;
   uint8_t* sb = c->sendbuf.as<uint8_t>();
   if ((rc0 = encode_segments(c, x, xo, nn, fof, sb, book, s.flen, st))) return rc0;
-  cudaMemcpyAsync(c->pinned + 192, s.flen, 8 * nn.size() + 8, cudaMemcpyDeviceToHost, st);
+  if (!nn.empty())
+    cudaMemcpyAsync(c->pinned + 192, s.flen, 8 * nn.size(), cudaMemcpyDeviceToHost, st);
   if ((ce = cudaStreamSynchronize(st)) != cudaSuccess) return (int)ce;
   std::vector<int64_t> flen(W, 0);
   for (size_t i = 0; i < seg_peer.size(); ++i) flen[seg_peer[i]] = (int64_t)c->pinned[192 + i];

@@ -816,7 +816,10 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
     const uint32_t h16 = (16u - mis) & 15u;
     const uint32_t head = run < h16 ? run : h16;
     if (tid < head) dst[tid] = esc_out[tid];
-    const uint32_t nbody = (run - head) >> 4;
+    // (with head > 0 the second load of the last 16-B word would read past
+    // the run: that word goes to the byte tail instead)
+    uint32_t nbody = (run - head) >> 4;
+    if (head && nbody && head + 16u * nbody + 16u > run) --nbody;
     uint4* d4 = reinterpret_cast<uint4*>(dst + head);
     const uint4* s4 = reinterpret_cast<const uint4*>(esc_out);
     const uint32_t sh = 8u * (head & 3u);
