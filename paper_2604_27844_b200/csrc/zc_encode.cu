@@ -462,21 +462,18 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
         s2 += f2_sum(c2);
       }
       const uint32_t cnt0 = __popc(esc0), cnt1 = __popc(esc1);
-      const uint32_t incl0 = warp_incl_scan(cnt0);
-      const uint32_t incl1 = warp_incl_scan(cnt1);
-      if (lane == 31) {
-        s_warp2[0][warp] = incl0;
-        s_warp2[1][warp] = incl1;
-      }
+      // both tiles' counts in one scan: tile 0 in the low 16 bits, tile 1 in
+      // the high (a tile holds <= 4096 escapes, so neither half carries)
+      const uint32_t inclp = warp_incl_scan(cnt0 | (cnt1 << 16));
+      const uint32_t incl0 = inclp & 0xFFFFu, incl1 = inclp >> 16;
+      if (lane == 31) s_warp2[0][warp] = inclp;
       __syncthreads();                                    // (B)
-      const uint32_t v0 = lane < kWarps ? s_warp2[0][lane] : 0u;
-      const uint32_t v1 = lane < kWarps ? s_warp2[1][lane] : 0u;
-      const uint32_t wi0 = warp_incl_scan<kWarps>(v0);
-      const uint32_t wi1 = warp_incl_scan<kWarps>(v1);
-      const uint32_t wbase0 = __shfl_sync(0xffffffffu, wi0 - v0, warp);
-      const uint32_t wbase1 = __shfl_sync(0xffffffffu, wi1 - v1, warp);
-      const uint32_t agg0 = __shfl_sync(0xffffffffu, wi0, kWarps - 1);
-      const uint32_t agg1 = __shfl_sync(0xffffffffu, wi1, kWarps - 1);
+      const uint32_t vp = lane < kWarps ? s_warp2[0][lane] : 0u;
+      const uint32_t wip = warp_incl_scan<kWarps>(vp);
+      const uint32_t wbasep = __shfl_sync(0xffffffffu, wip - vp, warp);
+      const uint32_t aggp = __shfl_sync(0xffffffffu, wip, kWarps - 1);
+      const uint32_t wbase0 = wbasep & 0xFFFFu, wbase1 = wbasep >> 16;
+      const uint32_t agg0 = aggp & 0xFFFFu, agg1 = aggp >> 16;
       const uint32_t lp0 = run + wbase0 + incl0 - cnt0;
       const uint32_t lp1 = run + agg0 + wbase1 + incl1 - cnt1;
       place_gi(k, esc0, lp0);
@@ -545,8 +542,9 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
             dst[i] = (uint8_t)v;
           }
         };
-        dense16s(st0, esc0, incl0 - cnt0, s_warp2[0][warp], lp0);
-        dense16s(st1, esc1, incl1 - cnt1, s_warp2[1][warp], lp1);
+        const uint32_t wtp = s_warp2[0][warp];            // this warp's packed totals
+        dense16s(st0, esc0, incl0 - cnt0, wtp & 0xFFFFu, lp0);
+        dense16s(st1, esc1, incl1 - cnt1, wtp >> 16, lp1);
       } else if (m) {
         const uint32_t a0 = smem_u32(ring + st0 * kStageBytes) + tid * (2 * kEPT);
         const uint32_t a1 = smem_u32(ring + st1 * kStageBytes) + tid * (2 * kEPT) - 32u;
