@@ -143,7 +143,7 @@ encode_lookback_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs,
     for (int j = 0; j < 4; ++j) {
       const uint32_t p = prmt(w[2 * j], w[2 * j + 1], 0x6420);   // low bytes
       const uint32_t q = prmt(w[2 * j], w[2 * j + 1], 0x7531);   // sign | e7..e1
-      sm[j] = (p & 0x7F7F7F7Fu) | (q & 0x80808080u);
+      sm[j] = bitsel(0x7F7F7F7Fu, p, q);   // one LOP3: (p & m) | (q & ~m)
     }
     // ---- exponent bytes (bf16.py:39-41), staged for the escape path -------
     {
@@ -411,7 +411,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
       for (int j = 0; j < 4; ++j) {
         const uint32_t p = prmt(w[2 * j], w[2 * j + 1], 0x6420);
         const uint32_t q = prmt(w[2 * j], w[2 * j + 1], 0x7531);
-        sm[j] = (p & 0x7F7F7F7Fu) | (q & 0x80808080u);
+        sm[j] = bitsel(0x7F7F7F7Fu, p, q);   // one LOP3: (p & m) | (q & ~m)
       }
       uint32_t A = 0, B = 0;
 #pragma unroll
@@ -615,7 +615,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     for (int j = 0; j < 4; ++j) {
       const uint32_t p = prmt(w[2 * j], w[2 * j + 1], 0x6420);
       const uint32_t q = prmt(w[2 * j], w[2 * j + 1], 0x7531);
-      sm[j] = (p & 0x7F7F7F7Fu) | (q & 0x80808080u);
+      sm[j] = bitsel(0x7F7F7F7Fu, p, q);   // one LOP3: (p & m) | (q & ~m)
     }
     // ---- codes -> plane bytes + escape mask (codec.py:281-289) ---------------
     uint32_t A = 0, B = 0;
