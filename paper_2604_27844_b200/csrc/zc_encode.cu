@@ -823,16 +823,44 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
     const uint32_t sh = 8u * (head & 3u);
     // body word i = scratch bytes [head + 16 i, head + 16 i + 16): words
     // q .. q + 4 of the pair (s4[i], s4[i + 1]), q = head / 4
+    // four words per thread per iteration: their loads are all in flight
+    // before the first store (one 16-B load per thread at a time left the
+    // copy latency-bound at ~3.6 TB/s on escape-heavy data)
+    constexpr int kU = 4;
     auto body = [&](auto qc) {
       constexpr int q = decltype(qc)::value;
-      for (uint32_t i = tid; i < nbody; i += kThreads) {
-        const uint4 a = __ldcs(s4 + i);
-        const uint4 b = head ? __ldcs(s4 + i + 1) : a;   // starts inside the run when head > 0
-        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        __stcs(d4 + i, make_uint4(__funnelshift_r(w[q], w[q + 1], sh),
-                                  __funnelshift_r(w[q + 1], w[q + 2], sh),
-                                  __funnelshift_r(w[q + 2], w[q + 3], sh),
-                                  __funnelshift_r(w[q + 3], w[q + 4], sh)));
+      // warp-uniform trip count: every lane takes part in the shuffles
+      for (uint32_t w0 = (uint32_t)(tid & ~31); w0 < nbody; w0 += kU * kThreads) {
+        const uint32_t i0 = w0 + (uint32_t)lane;
+        uint4 a[kU], b[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t i = i0 + u * kThreads;
+          // (word nbody too when head > 0: the last body word's neighbour,
+          // inside the run by the nbody rule above)
+          a[u] = (i < nbody || (head && i == nbody)) ? __ldcs(s4 + i) : make_uint4(0, 0, 0, 0);
+        }
+        // word i + 1 is the next lane's word i (lane 31 loads it itself)
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t i = i0 + u * kThreads;
+          b[u].x = __shfl_down_sync(0xffffffffu, a[u].x, 1);
+          b[u].y = __shfl_down_sync(0xffffffffu, a[u].y, 1);
+          b[u].z = __shfl_down_sync(0xffffffffu, a[u].z, 1);
+          b[u].w = __shfl_down_sync(0xffffffffu, a[u].w, 1);
+          if (head && lane == 31 && i < nbody) b[u] = s4[i + 1];   // inside the run when head > 0
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t i = i0 + u * kThreads;
+          if (i < nbody) {
+            const uint32_t w[8] = {a[u].x, a[u].y, a[u].z, a[u].w, b[u].x, b[u].y, b[u].z, b[u].w};
+            __stcs(d4 + i, make_uint4(__funnelshift_r(w[q], w[q + 1], sh),
+                                      __funnelshift_r(w[q + 1], w[q + 2], sh),
+                                      __funnelshift_r(w[q + 2], w[q + 3], sh),
+                                      __funnelshift_r(w[q + 3], w[q + 4], sh)));
+          }
+        }
       }
     };
     switch (head >> 2) {

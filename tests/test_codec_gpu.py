@@ -174,6 +174,24 @@ def test_escape_density_mix_two_pass_against_oracle(gs):
     assert np.array_equal(host_words(zc.decompress(zc.parse(frame))), w)
 
 
+@pytest.mark.parametrize("kind,n", [("lognormal2", 4096 * 1100 + 5), ("mix_x1000", 4096 * 1500 + 77),
+                                    ("lognormal2", 4096 * 2048), ("mix_n10", 4096 * 1031 + 4095)])
+def test_escape_heavy_runs_match_oracle(kind, n):
+    # C4 outlier mixes (58-96 % escapes) through the measured-codebook
+    # encoder: runs of several thousand escapes take the run fix-up's
+    # shifted 16-B copy (any frame alignment of the run, warp-uniform loop)
+    # and the dense staging of pass 1; frames byte-exact against the oracle
+    w = zo.outlier_mix(n, kind, seed=n % 97)
+    x = torch.from_numpy(w.view(np.int16)).cuda()
+    book = zc.codebook_for(x)
+    assert book.entries == zo.book_for(w)
+    frame = zc.serialize(zc.compress(x, book))
+    assert frame == zo.encode(w, book.entries)
+    frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    _, _, flen = engine.encode_measured(x, [(0, n)], 9, frames, [0])
+    assert bytes(frames[:int(flen.item())].cpu().numpy()) == frame
+
+
 @pytest.mark.parametrize("n", [1 << 27, 218112000 // 8, 5 * 4096 * 4096 + 3])
 def test_large_round_trip_properties(n):
     # size-independent properties at benchmark scale: decode(encode(x)) == x,
