@@ -384,11 +384,16 @@ cudaError_t launch_codebook_modal(const uint16_t* x, const StatSegs& segs, int64
 // ---- speculative encoder support (launch_encode_auto) -------------------------
 // Guess for the speculative encoder: the analytic codebook of packed-fp32
 // sums over a uniform element sample -- one 32-B sector (16 words) every
-// kGuessStride words, i.e. 1/128 of the bytes, spread over the whole input
+// kGuessStride words, i.e. 1/256 of the bytes (one sector per tile: half the
+// DRAM lines of 1/128 for a sigma estimate still within ~0.1 %), spread over the whole input
 // so that no region is over-weighted (a tile sample would be fooled by a
 // small cluster, e.g. the RMSNorm vectors at the end of a layer shard).  No
 // certificate: a wrong guess only costs a re-encode.
-constexpr int kGuessStride = 2048;
+#ifndef ZC_GSTRIDE
+#define ZC_GSTRIDE 4096
+#endif
+constexpr int kGuessStride = ZC_GSTRIDE;
+static_assert(kTile % kGuessStride == 0, "probes per tile");
 struct GuessPartial {
   double s1, s2, cnt;
 };
