@@ -7,6 +7,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include "zc_common.cuh"
+#include "zc_stats.cuh"
 
 namespace zc {
 cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, void*, uint8_t*,
@@ -148,7 +149,9 @@ int zc_codebook_measured(const uint16_t* x, const int64_t* seg_off, const int64_
   }
   s.nseg = k;
   if (k > 0 && !x) return kStatusBadArg;
-  if (128 + 32 * s.tile_start[k] > ws_bytes) return kStatusWorkspace;
+  // (the numpy-order sigma passes use the area at kNpWsOff)
+  if (128 + 32 * s.tile_start[k] > ws_bytes || kNpWsOff + kNpArea > ws_bytes)
+    return kStatusWorkspace;
   return status_of(launch_codebook_measured(x, s, total, ws, book_dev, result_dev, flags & 1,
                                             stream));
 }

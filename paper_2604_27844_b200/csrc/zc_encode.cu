@@ -895,9 +895,10 @@ static int grid_for(const void* fn, int threads, size_t dyn_smem) {
 }
 
 constexpr int64_t kSpecArea = 512 * 1024;   // sampled + exact partials, guess book, flag
+static_assert(kNpWsOff == 256 + 8 * 4096 + kSpecArea, "numpy-exact sigma area follows the spec area");
 
 int64_t encode_workspace_bytes(int64_t ntiles) {
-  return 256 + 8 * 4096 + kSpecArea + (int64_t)kTile * ntiles;
+  return 256 + 8 * 4096 + kSpecArea + kNpArea + (int64_t)kTile * ntiles;
 }
 
 static RunPlan make_plan(const EncodeSegs& segs, int cap1) {
@@ -942,7 +943,7 @@ static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, co
                                    uint64_t* frame_len, const SpecOut* spec,
                                    const uint8_t* skip_if_same, cudaStream_t st) {
   uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
-  uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea;
+  uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea + kNpArea;
   const bool timed = skip_if_same == nullptr;   // not the conditional re-encode
   if (timed) prof_mark(kProfEncode, false, st);
   if (spec)
@@ -1001,7 +1002,7 @@ cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, 
 cudaError_t launch_guess(const uint16_t*, const StatSegs&, void*, unsigned*, uint8_t*,
                          cudaStream_t);
 cudaError_t launch_exact_if_needed(const uint16_t*, const StatSegs&, int64_t, Partial*, unsigned*,
-                                   uint8_t*, double*, const int*, int, cudaStream_t);
+                                   uint8_t*, double*, const int*, int, void*, cudaStream_t);
 
 // Measured codebook + encode.  Large inputs take the speculative path:
 //   1. guess_kernel: a codebook guessed from a uniform 1/128 sample;
@@ -1063,7 +1064,8 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   const SpecOut so{run_sums, counters + 1, total, book, result, need};
   e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, &so, nullptr, st);
   if (e != cudaSuccess) return e;
-  e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms, st);
+  e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms,
+                             w8, st);
   if (e != cudaSuccess) return e;
   return launch_two_pass(x, segs, rp2, book, frames, w8, frame_len, nullptr, guess, st);
 }

@@ -339,10 +339,252 @@ __global__ void mode_kernel(const unsigned long long* __restrict__ hist, int64_t
 // fewer, and its f64 work is negligible at this size.
 constexpr int64_t kSmallExactTiles = 16;
 
+// ---- numpy-exact sigma ---------------------------------------------------------
+// The reference's sigma is np.std over the finite values (bf16.py:103), i.e.
+// numpy's _var: mean = (0.0 + S) / m, ret = (0.0 + Q) / m, sigma = sqrt(ret),
+// with S = pairwise_sum(v), Q = pairwise_sum((v - mean)^2) and numpy's
+// pairwise_sum (numpy/_core/src/umath/loops_utils.h.src, np.add.reduce of a
+// contiguous 1-D float64 array in one inner-loop call): n < 8: 0.0 plus the
+// elements in order; n <= 128: eight accumulators r[j] = a[j], r[j] += a[i+j]
+// for i = 8, 16, .. < n - n % 8, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then
+// the remaining elements in order; n > 128: the sums of the halves split at
+// n/2 - (n/2) % 8.  These kernels evaluate exactly that tree with IEEE
+// round-to-nearest adds (no contraction), so sigma is bit-identical to the
+// reference when every element is finite (the compacted array is then x
+// itself); with non-finite elements the exact Chan pass's value stays.
+// The tree's top kNpK levels are split over 2^kNpK threads: thread t owns
+// the node reached by t's bits (MSB first) if t is that node's leftmost
+// index; it evaluates its subtree depth first (explicit stack), and the last
+// CTA combines the owners bottom-up (node = left + right).
+constexpr int kNpLeaf = 128;
+
+__device__ __forceinline__ int64_t np_left(int64_t n) {
+  const int64_t n2 = n / 2;
+  return n2 - n2 % 8;
+}
+
+// forward-only reader of the concatenated segments as float64
+struct NpCursor {
+  const uint16_t* x;
+  const StatSegs* segs;
+  int s;
+  int64_t lo, hi;                   // concatenated range of segment s
+  __device__ void init(const uint16_t* x_, const StatSegs* sg, int64_t e) {
+    x = x_;
+    segs = sg;
+    s = 0;
+    lo = 0;
+    hi = sg->n[0];
+    seek(e);
+  }
+  __device__ __forceinline__ void seek(int64_t e) {
+    while (e >= hi && s + 1 < segs->nseg) {
+      ++s;
+      lo = hi;
+      hi += segs->n[s];
+    }
+  }
+  __device__ __forceinline__ double val(int64_t e) {
+    seek(e);
+    return (double)__uint_as_float((uint32_t)x[segs->x_off[s] + (e - lo)] << 16);
+  }
+  // elements e .. e + 7
+  __device__ __forceinline__ void val8(int64_t e, double (&v)[8]) {
+    seek(e);
+    const uint16_t* p = x + segs->x_off[s] + (e - lo);
+    if (e + 8 <= hi && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const uint4 q = __ldcg(reinterpret_cast<const uint4*>(p));
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[2 * j] = (double)__uint_as_float(w[j] << 16);
+        v[2 * j + 1] = (double)__uint_as_float(w[j] & 0xFFFF0000u);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = val(e + j);
+    }
+  }
+};
+
+template <int kPass>
+__device__ __forceinline__ double np_term(double v, double mean) {
+  if (kPass == 0) return v;
+  const double d = __dsub_rn(v, mean);
+  return __dmul_rn(d, d);
+}
+
+template <int kPass>
+__device__ double np_leaf(NpCursor& c, int64_t start, int64_t n, double mean) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, np_term<kPass>(c.val(start + i), mean));
+    return r;
+  }
+  double r[8], v[8];
+  c.val8(start, v);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = np_term<kPass>(v[j], mean);
+  int64_t i = 8;
+  const int64_t lim = n - n % 8;
+  for (; i < lim; i += 8) {
+    c.val8(start + i, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], np_term<kPass>(v[j], mean));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, np_term<kPass>(c.val(start + i), mean));
+  return res;
+}
+
+// pairwise_sum of [start, start + n): post-order walk with an explicit stack
+template <int kPass>
+__device__ double np_subtree(NpCursor& c, int64_t start, int64_t n, double mean) {
+  struct Fr {
+    int64_t start, n;
+    double lv;
+    int st;                              // 0 new, 1 left pending, 2 right pending
+  };
+  Fr stk[32];                            // depth <= log2(2^32 / 128) + 1
+  int sp = 0;
+  stk[sp++] = Fr{start, n, 0.0, 0};
+  double ret = 0.0;
+  bool have = false;                     // a finished child's value is in ret
+  while (sp > 0) {
+    Fr& f = stk[sp - 1];
+    if (have) {
+      if (f.st == 1) {                   // left done: keep it, descend right
+        f.lv = ret;
+        f.st = 2;
+        have = false;
+        const int64_t L = np_left(f.n);
+        stk[sp++] = Fr{f.start + L, f.n - L, 0.0, 0};
+      } else {                           // right done: left + right, up one level
+        ret = __dadd_rn(f.lv, ret);
+        --sp;
+      }
+      continue;
+    }
+    if (f.n <= kNpLeaf) {
+      ret = np_leaf<kPass>(c, f.start, f.n, mean);
+      --sp;
+      have = true;
+      continue;
+    }
+    f.st = 1;
+    stk[sp++] = Fr{f.start, np_left(f.n), 0.0, 0};
+  }
+  return ret;
+}
+
+// grid = kNpOwners / kThreads.  Runs only when the exact pass saw every
+// element finite and sigma > 0 (and, behind the certificate, when it failed).
+// grid = kNpOwners / kThreads (one owner block of 256 per CTA).
+template <int kPass>
+__global__ void __launch_bounds__(kThreads)
+np_sigma_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t total,
+                NpWs* __restrict__ w, unsigned* __restrict__ done, uint8_t* __restrict__ book,
+                double* __restrict__ result) {
+  if (total < 1 || !(__ldcg(result + 1) == (double)total) || !(__ldcg(result) > 0.0)) return;
+  constexpr int kLv = 8;                              // log2(kThreads)
+  static_assert((1 << kLv) == kThreads, "one owner index per thread");
+  const int tid = threadIdx.x;
+  const int t = (int)blockIdx.x * kThreads + tid;
+  const double mean = kPass ? __ldcg(&w->mean) : 0.0;
+  int64_t start = 0, n = total;
+  int d = 0;
+  bool owner = true;
+  for (; d < kNpK; ++d) {
+    if (n <= kNpLeaf) {
+      owner = (t & ((1 << (kNpK - d)) - 1)) == 0;
+      break;
+    }
+    const int64_t L = np_left(n);
+    if ((t >> (kNpK - 1 - d)) & 1) {
+      start += L;
+      n -= L;
+    } else {
+      n = L;
+    }
+  }
+  __shared__ double s_val[kThreads];
+  __shared__ int8_t s_dep[kThreads];
+  double mine = 0.0;
+  if (owner) {
+    NpCursor c;
+    c.init(x, &segs, start);
+    mine = np_subtree<kPass>(c, start, n, mean);
+  }
+  s_val[tid] = mine;
+  s_dep[tid] = owner ? (int8_t)d : (int8_t)-1;
+  w->depth[t] = s_dep[tid];
+  __syncthreads();
+  // node = left + right, bottom-up, in place at each node's leftmost index:
+  // the CTA's 256 owner indices are one subtree (depth kNpK - 8), combined in
+  // shared memory; the last CTA combines the CTAs' values above it
+  for (int dd = kNpK - 1; dd >= kNpK - kLv; --dd) {
+    const int step = 1 << (kNpK - dd);
+    if ((tid & (step - 1)) == 0 && s_dep[tid] > dd)
+      s_val[tid] = __dadd_rn(s_val[tid], s_val[tid + step / 2]);
+    __syncthreads();
+  }
+  if (tid == 0) w->parts[t] = s_val[0];
+  __shared__ bool s_last;
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int dd = kNpK - kLv - 1; dd >= 0; --dd) {
+    for (int p = tid; p < (1 << dd); p += kThreads) {
+      const int t0 = p << (kNpK - dd);
+      if (__ldcg(&w->depth[t0]) > dd)
+        w->parts[t0] = __dadd_rn(__ldcg(&w->parts[t0]),
+                                 __ldcg(&w->parts[t0 + (1 << (kNpK - dd - 1))]));
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *done = 0;                                        // for the next pass / call
+    const double v = __ddiv_rn(__dadd_rn(0.0, __ldcg(&w->parts[0])), (double)total);
+    if (kPass == 0) {
+      w->mean = v;
+    } else {
+      const double sigma = __dsqrt_rn(v);
+      result[0] = sigma;
+      if (isfinite(sigma) && sigma > 0.0) {
+        write_window(book, derive_base(sigma));
+        result[2] = 1.0;
+      }
+    }
+  }
+}
+
+// both passes behind the exact statistic (result / book already hold its
+// answer); `ws` is the caller's workspace (np area at kNpWsOff).  Run for
+// the exact statistic (measure_sigma's flag): codebook_for's certified path
+// and the speculative encoder keep the Chan pass, whose codebook is the
+// reference's except within ~1e-15 relative of a flip threshold, without
+// two extra launches per call.
+cudaError_t launch_np_sigma(const uint16_t* x, const StatSegs& segs, int64_t total, void* ws,
+                            unsigned* done, uint8_t* book, double* result, cudaStream_t st) {
+  if (total < 1) return cudaSuccess;
+  NpWs* w = reinterpret_cast<NpWs*>(reinterpret_cast<uint8_t*>(ws) + kNpWsOff);
+  np_sigma_kernel<0><<<kNpOwners / kThreads, kThreads, 0, st>>>(x, segs, total, w, done, book,
+                                                                result);
+  np_sigma_kernel<1><<<kNpOwners / kThreads, kThreads, 0, st>>>(x, segs, total, w, done, book,
+                                                                result);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, int64_t total,
                                      void* ws, uint8_t* book, double* result, int exact,
                                      cudaStream_t st, bool zeroed) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
+  const int asked = exact;            // measure_sigma's request: numpy's order too
   if (ntiles <= kSmallExactTiles) exact = 1;
   uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
   Partial* parts = reinterpret_cast<Partial*>(w8 + 128);
@@ -364,6 +606,12 @@ cudaError_t launch_codebook_measured(const uint16_t* x, const StatSegs& segs, in
     }
     stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(
         x, segs, parts, done, total, book, result, exact ? nullptr : need);
+    // the reference's own summation order for sigma (all-finite inputs)
+    if (asked == 1) {
+      cudaError_t e = launch_np_sigma(x, segs, total, ws, reinterpret_cast<unsigned*>(w8 + 76),
+                                      book, result, st);
+      if (e != cudaSuccess) return e;
+    }
   } else {
     finalize_kernel<<<1, kThreads, 0, st>>>(parts, 0, total, book, result);
   }
@@ -493,13 +741,14 @@ cudaError_t launch_guess(const uint16_t* x, const StatSegs& segs, void* parts, u
 cudaError_t launch_exact_if_needed(const uint16_t* x, const StatSegs& segs, int64_t total,
                                    Partial* parts, unsigned* done, uint8_t* book,
                                    double* result, const int* need, int grid_limit,
-                                   cudaStream_t st) {
+                                   void* np_ws, cudaStream_t st) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
   int64_t grid = stats_grid_cap();
   if (grid > grid_limit) grid = grid_limit;
   if (grid > ntiles) grid = ntiles;
   stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(
       x, segs, parts, done, total, book, result, need);
+  (void)np_ws;
   return cudaGetLastError();
 }
 
@@ -516,6 +765,8 @@ cudaError_t preload_stats() {
   cudaFuncGetAttributes(&a, (const void*)mode_kernel);
   cudaFuncGetAttributes(&a, (const void*)stats_kernel);
   cudaFuncGetAttributes(&a, (const void*)sums_kernel);
+  cudaFuncGetAttributes(&a, (const void*)np_sigma_kernel<0>);
+  cudaFuncGetAttributes(&a, (const void*)np_sigma_kernel<1>);
   stats_grid_cap();
   sums_grid_cap();
   return cudaGetLastError();

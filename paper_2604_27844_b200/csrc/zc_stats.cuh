@@ -329,4 +329,20 @@ __device__ inline void certify_block(const SumPartial* parts, int64_t nparts, in
   *need = decided ? 0 : 1;
 }
 
+// ---- numpy-exact sigma (zc_stats.cu np_sigma_kernel) ---------------------------
+// Workspace of the two passes: the mean of pass 0 and the subtree sums of the
+// 2^kNpK owners of the pairwise tree's top levels.  It sits behind the
+// encoder's run totals and speculative area (zc_encode.cu: 256 + 32 KB +
+// 512 KB), in front of the encoder scratch.
+constexpr int kNpK = 17;
+constexpr int kNpOwners = 1 << kNpK;
+struct NpWs {
+  double mean;
+  double pad[7];
+  double parts[kNpOwners];
+  int8_t depth[kNpOwners];       // owner's node depth, -1 = not an owner
+};
+constexpr int64_t kNpArea = ((int64_t)sizeof(NpWs) + 4095) / 4096 * 4096;
+constexpr int64_t kNpWsOff = 256 + 8 * 4096 + 512 * 1024;
+
 }  // namespace zc

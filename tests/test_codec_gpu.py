@@ -57,6 +57,40 @@ def test_sigma_cases(golden_meta):
         assert list(zc.codebook_for(w).entries) == c["book"], c
 
 
+def _np_sigma(words: np.ndarray) -> float:
+    """The reference's measure_sigma (bf16.py:88-103): np.std of the finite
+    values as float64."""
+    v = (words.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return float(np.std(v[np.isfinite(v)]))
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 8, 9, 100, 127, 128, 129, 136, 1000, 8195, 100003,
+                               4096 * 300 + 17, (1 << 20) + 5, 1 << 24])
+def test_sigma_is_bit_identical_to_numpy(n):
+    # all-finite inputs: numpy's pairwise summation order reproduced on the
+    # device (np_sigma_kernel), so measure_sigma is the reference's float
+    for s, seed in ((0.02, n), (1.0, n + 1), (3e-4, n + 2)):
+        w = zo.gaussian(n, s, seed)
+        if n > 2:
+            w[: n // 3] = zo.from_f64(np.random.default_rng(seed).standard_normal(n // 3) * 7.0 + 3.0)
+        got = zc.measure_sigma(w)
+        assert got == _np_sigma(w), (n, s, got, _np_sigma(w))
+
+
+def test_sigma_bit_identical_over_segments():
+    # the all-to-all statistic spans several chunks (collectives.py:230-242):
+    # the concatenation's pairwise order crosses chunk boundaries
+    rng = np.random.default_rng(5)
+    chunks = [zo.gaussian(c, 0.02, seed=c) for c in (4096 * 3 + 5, 77, 100003, 9)]
+    buf = np.concatenate(chunks)
+    x = torch.from_numpy(buf.view(np.int16)).cuda()
+    offs = np.concatenate([[0], np.cumsum([c.size for c in chunks])[:-1]]).tolist()
+    segs = [(int(o), int(c.size)) for o, c in zip(offs, chunks)]
+    _, result = engine.measured_codebook(engine.words_view(x), segs, exact=True)
+    assert float(result[0].item()) == _np_sigma(buf)
+    assert rng is not None
+
+
 def test_sigma_special_values():
     assert zc.measure_sigma(np.full(10, 0x3F80, np.uint16)) == 0.0
     assert zc.measure_sigma(zo.from_f64(np.array([-1.0, 1.0]))) == 1.0
