@@ -61,6 +61,11 @@ err = engine.decode([frames.data_ptr() + o for o in offs], [0, 0], None, [c for 
                     [0, segs[0][1]])
 assert (err.cpu() == engine.ERR_OK).all()
 checks += 1
+# numpy-order sigma (measure_sigma: exact Chan pass + np_sigma_kernel passes)
+for n in (5, 1000, 4096 * 40 + 3):
+    x = words(n)
+    zc.measure_sigma(x)
+checks += 1
 # modal fallback and explicit sigma
 x = words(10_000)
 zc.codebook_for(x, sigma=0.0)
