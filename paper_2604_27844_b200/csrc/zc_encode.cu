@@ -1002,7 +1002,7 @@ cudaError_t launch_codebook_measured(const uint16_t*, const StatSegs&, int64_t, 
 cudaError_t launch_guess(const uint16_t*, const StatSegs&, void*, unsigned*, uint8_t*,
                          cudaStream_t);
 cudaError_t launch_exact_if_needed(const uint16_t*, const StatSegs&, int64_t, Partial*, unsigned*,
-                                   uint8_t*, double*, const int*, int, void*, cudaStream_t);
+                                   uint8_t*, double*, const int*, int, cudaStream_t);
 
 // Measured codebook + encode.  Large inputs take the speculative path:
 //   1. guess_kernel: a codebook guessed from a uniform 1/128 sample;
@@ -1064,8 +1064,7 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   const SpecOut so{run_sums, counters + 1, total, book, result, need};
   e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, &so, nullptr, st);
   if (e != cudaSuccess) return e;
-  e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms,
-                             w8, st);
+  e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms, st);
   if (e != cudaSuccess) return e;
   return launch_two_pass(x, segs, rp2, book, frames, w8, frame_len, nullptr, guess, st);
 }

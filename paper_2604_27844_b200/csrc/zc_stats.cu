@@ -741,14 +741,13 @@ cudaError_t launch_guess(const uint16_t* x, const StatSegs& segs, void* parts, u
 cudaError_t launch_exact_if_needed(const uint16_t* x, const StatSegs& segs, int64_t total,
                                    Partial* parts, unsigned* done, uint8_t* book,
                                    double* result, const int* need, int grid_limit,
-                                   void* np_ws, cudaStream_t st) {
+                                   cudaStream_t st) {
   const int64_t ntiles = segs.tile_start[segs.nseg];
   int64_t grid = stats_grid_cap();
   if (grid > grid_limit) grid = grid_limit;
   if (grid > ntiles) grid = ntiles;
   stats_kernel<<<(unsigned)grid, kThreads, stats_dyn_smem(), st>>>(
       x, segs, parts, done, total, book, result, need);
-  (void)np_ws;
   return cudaGetLastError();
 }
 
