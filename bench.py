@@ -767,6 +767,7 @@ def run_grad_mix(args):
         torch.cuda.synchronize()
         assert int(err.item()) == engine.ERR_OK and torch.equal(out, w)
         F = int(flen.item())
+        zc = int.from_bytes(bytes(frames[16:24].cpu().numpy()), "little")   # header zero_count
         ge, gd = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(ge):
             enc()
@@ -786,12 +787,83 @@ def run_grad_mix(args):
             times[name] = a.elapsed_time(b) / args.steps
         print(json.dumps({
             "metric": METRIC, "workload": f"c4 gradient {kind}", "n": n,
-            "ratio": 2 * n / F, "escape_rate": None,
+            "ratio": 2 * n / F, "escape_rate": zc / n,
             "codebook_encode_GBps": 2 * n / (times["encode"] / 1e3) / 1e9,
             "decode_GBps": 2 * n / (times["decode"] / 1e3) / 1e9,
             "encode_ms": times["encode"], "decode_ms": times["decode"],
             "note": "GB/s of uncompressed BF16; ratio < 1 means the frame expands "
                     "(the switcher then picks the raw collective)"}), flush=True)
+
+
+C1_FRAME_SHA256 = "9d65816bae340834eadc3a854b9173fbc68db6ec744dafa3b9d8e294c3d9fdae"
+
+
+def run_c1(args):
+    """BASELINE configs[0] on the GPU beside its CPU reference path: the
+    codec round trip of the 2^24-element N(0, 0.02^2) tensor (frame digest
+    checked against SURVEY Appendix B) and the simulated W=2 zip_all_gather
+    (run_ranks(2, ...) with timed_call, here two thread ranks of the native
+    engine sharing the GPU; shards rng([0, rank]) of 2^23 elements)."""
+    import hashlib
+    import numpy as np
+    import torch
+    from oracle import zc_oracle as zo
+    from paper_2604_27844_b200 import collectives as coll, engine
+    from paper_2604_27844_b200.transport import run_ranks
+    dev = torch.device("cuda", 0)
+    n = 1 << 24
+    host = zo.from_f64(np.random.default_rng(0).standard_normal(n) * 0.02)
+    w = torch.from_numpy(host.view(np.int16)).to(dev)
+    frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device=dev)
+    out = torch.empty_like(w)
+    flen = torch.empty(1, dtype=torch.int64, device=dev)
+    err = torch.empty(1, dtype=torch.int32, device=dev)
+    enc = lambda: engine.encode_measured(w, [(0, n)], 9, frames, [0], flen)  # noqa: E731
+    dec = lambda: engine.decode([frames.data_ptr()], [0], None, [n], out, [0], err=err)  # noqa: E731
+    enc()
+    dec()
+    torch.cuda.synchronize()
+    F = int(flen.item())
+    digest = hashlib.sha256(frames[:F].cpu().numpy().tobytes()).hexdigest()
+    assert int(err.item()) == engine.ERR_OK and torch.equal(out, w)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        enc()
+        dec()
+    for _ in range(args.warmup):
+        g.replay()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(args.steps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    rt_ms = a.elapsed_time(b) / args.steps
+    shard = 1 << 23
+
+    def body(comm):
+        local = torch.from_numpy(zo.rank_gaussian(comm.rank, shard, s=0.02).view(np.int16)).to(dev)
+        ref = coll.reference_all_gather(comm, local)
+        for _ in range(args.warmup):
+            coll.zip_all_gather(comm, local)
+        best = None
+        for _ in range(args.steps):
+            got, t = coll.timed_call(comm, lambda: coll.zip_all_gather(comm, local))
+            best = t if best is None else min(best, t)
+        assert torch.equal(got, ref)
+        return best
+    ag_s = max(run_ranks(2, body))
+    cpu = c1_simulated_allgather() if not args.no_cpu_baseline else None
+    print(json.dumps({
+        "metric": METRIC, "workload": "c1 codec round trip 2^24 + simulated W=2 all-gather",
+        "n": n, "frame_bytes": F, "ratio": 2 * n / F, "frame_sha256_matches_reference":
+        digest == C1_FRAME_SHA256, "roundtrip_ms": rt_ms,
+        "roundtrip_GBps": 2 * n / (rt_ms / 1e3) / 1e9,
+        "simulated_w2_allgather_ms": ag_s * 1e3,
+        "simulated_w2_note": "two thread ranks sharing one GPU (native engine, host rendezvous "
+                             "between them): a latency figure, not an NVLink number",
+        "cpu_reference_w2_allgather": cpu}), flush=True)
 
 
 def _init_dist(args):
@@ -1113,7 +1185,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the N=1 step eagerly (default: CUDA graph replays)")
     ap.add_argument("--workload", default="layer_ag",
-                    choices=["layer_ag", "moe_a2a", "grad_mix", "sweep", "imbalance"],
+                    choices=["layer_ag", "moe_a2a", "grad_mix", "sweep", "imbalance", "c1"],
                     help="layer_ag: the headline line (configs[1]); moe_a2a: configs[2]; "
                          "grad_mix: configs[3]; sweep: configs[4]")
     ap.add_argument("--tokens", type=int, default=4096, help="moe_a2a tokens per rank")
@@ -1135,6 +1207,8 @@ def main():
         run_reference(args)
     elif args.workload == "grad_mix":
         run_grad_mix(args)
+    elif args.workload == "c1":
+        run_c1(args)
     elif args.workload == "moe_a2a":
         run_moe_a2a(args)
     elif args.workload == "sweep":
