@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import threading
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import torch
 
@@ -318,16 +318,85 @@ class HubCommunicator(Communicator):
         self.hub.sync(self.rank)
 
 
-def run_ranks(world_size: int, fn, device=None, timeout: float = DEFAULT_TIMEOUT,
-              native: bool | None = None) -> list:
+MODE_PARALLEL = "full-p2p-parallel"
+MODE_SERIALIZED = "serialized-links"
+RENDEZVOUS_ENV = "ZIPCOLL_RENDEZVOUS"
+
+
+@dataclass
+class SimProfile:
+    """The reference's simulated-fabric parameters (transport.py:96-126),
+    accepted for API compatibility.  The virtual-clock transport itself is
+    not part of this build (out of scope) -- collectives here
+    are timed on the device -- so run_ranks(..., transport="sim") raises."""
+
+    bandwidth: float = 1e9
+    latency: float = 10e-6
+    mode: str = MODE_PARALLEL
+    ready_times: dict = field(default_factory=dict)
+    link_bandwidth: dict = field(default_factory=dict)
+    link_latency: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if self.bandwidth <= 0 or any(b <= 0 for b in self.link_bandwidth.values()):
+            raise ValueError("bandwidth must be positive")
+        if self.latency < 0 or any(v < 0 for v in self.link_latency.values()):
+            raise ValueError("latency must be nonnegative")
+        if any(t < 0 for t in self.ready_times.values()):
+            raise ValueError("ready_time must be nonnegative")
+        if self.mode not in (MODE_PARALLEL, MODE_SERIALIZED):
+            raise ValueError(f"unknown concurrency mode {self.mode!r}")
+
+
+def connect_tcp(world_size: int, rank: int, rendezvous: str | None = None,
+                timeout: float = DEFAULT_TIMEOUT) -> Communicator:
+    """Reference connect_tcp (transport.py:669-671): this rank joins a group
+    of ``world_size`` ranks meeting at ``rendezvous`` ("host:port", else
+    $ZIPCOLL_RENDEZVOUS).  Here the meeting is torch.distributed's TCP
+    store and the group is NCCL when a GPU is visible (one process per GPU,
+    device = rank modulo the visible GPUs; the native engine then runs over
+    NVLink), gloo otherwise."""
+    import datetime
+    import os
+    import socket
+    import torch.distributed as dist
+    rendezvous = rendezvous or os.environ.get(RENDEZVOUS_ENV)
+    if world_size > 1 and not rendezvous:
+        raise TransportError(f"tcp transport needs a rendezvous address ({RENDEZVOUS_ENV})")
+    if not rendezvous:
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            rendezvous = f"127.0.0.1:{sk.getsockname()[1]}"
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        torch.cuda.set_device(rank % torch.cuda.device_count())
+    try:
+        dist.init_process_group(backend, init_method=f"tcp://{rendezvous}",
+                                world_size=world_size, rank=rank,
+                                timeout=datetime.timedelta(seconds=timeout))
+    except Exception as exc:  # noqa: BLE001 - the reference's error class
+        raise TransportError(f"tcp rendezvous at {rendezvous} failed: {exc}") from exc
+    return DistCommunicator()
+
+
+def run_ranks(world_size: int, fn, transport: str = "loopback",
+              sim_profile: SimProfile | None = None, timeout: float = DEFAULT_TIMEOUT, *,
+              device=None, native: bool | None = None) -> list:
     """Run fn(comm) on ``world_size`` in-process thread ranks sharing one GPU
     (or ``device`` per rank when a list is given); results by rank
-    (reference run_ranks, transport.py:635-666).  The first failure aborts
-    the hub so peers error out instead of hanging, and is re-raised.
+    (reference run_ranks, transport.py:635-666, same positional arguments).
+    The first failure aborts the hub so peers error out instead of hanging,
+    and is re-raised.  ``transport`` "loopback" (the reference's in-process
+    hub) is the thread-rank hub here; "sim" (virtual clock) is not provided.
 
     ``native`` (default: up to 64 ranks) gives every rank a native
     communicator of one in-process group, so the collectives run the C++
     engine exactly as NCCL ranks do; False keeps the generic protocols."""
+    if transport == "sim" or sim_profile is not None:
+        raise TransportError("the simulated (virtual-clock) transport is not part of the B200 "
+                             "build: collectives are timed on the device")
+    if transport != "loopback":
+        raise ValueError(f"unknown transport {transport!r}")
     hub = _Hub(world_size)
     results = [None] * world_size
     failures = []

@@ -106,3 +106,49 @@ def test_exchange_sizes_transpose_over_gloo():
         peer = 1 - r
         assert recv == [50 + peer] * (3 + peer)
         assert scal == [0.5, 1.5]
+
+
+def _tcp_worker(rank, world, addr, q):
+    from paper_2604_27844_b200 import connect_tcp
+    comm = connect_tcp(world, rank, addr, timeout=60)
+    got = comm.exchange_sizes([10 * rank + p for p in range(world)])
+    q.put((rank, comm.rank, comm.world_size, comm.backend, got))
+    import torch.distributed as dist
+    dist.destroy_process_group()
+
+
+def test_connect_tcp_gloo_rendezvous():
+    """Reference connect_tcp (transport.py:669-671) over torch.distributed's
+    TCP store: two processes meet at host:port and run the size exchange."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    addr = f"127.0.0.1:{_free_port()}"
+    procs = [ctx.Process(target=_tcp_worker, args=(r, world, addr, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((v[0], v[1:]) for v in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        rank, ws, backend, got = res[r]
+        assert (rank, ws, backend) == (r, world, "gloo")
+        assert got == [10 * p + r if p != r else 10 * r + r for p in range(world)]
+
+
+def test_sim_profile_validation_and_sim_transport_absent():
+    """SimProfile keeps the reference's validation (transport.py:96-126); the
+    virtual-clock transport itself is out of scope and fails loudly."""
+    from paper_2604_27844_b200 import SimProfile, TransportError, run_ranks
+    SimProfile(bandwidth=2e9, latency=0.0, mode="serialized-links")
+    for bad in (dict(bandwidth=0), dict(latency=-1), dict(mode="x"),
+                dict(ready_times={0: -1.0}), dict(link_bandwidth={(0, 1): 0})):
+        with pytest.raises(ValueError):
+            SimProfile(**bad)
+    with pytest.raises(TransportError):
+        run_ranks(2, lambda c: None, "sim", SimProfile())
+    with pytest.raises(ValueError):
+        run_ranks(2, lambda c: None, "carrier-pigeon")
+    with pytest.raises(TransportError):
+        from paper_2604_27844_b200 import connect_tcp
+        connect_tcp(2, 0, None)
