@@ -118,6 +118,18 @@ __device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Programmatic dependent launch (launch attribute ProgrammaticStreamSerialization):
+// a dependent grid may be scheduled once every CTA of this grid has issued
+// launch_dependents (or exited); grid_dep_wait blocks until the prerequisite
+// grid has completed and its writes are visible.  Both are no-ops in a grid
+// launched without the attribute.
+__device__ __forceinline__ void grid_dep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void grid_dep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // Read-once global loads (non-coherent path, no L1 allocation).  Not
 // volatile: the compiler may batch and reorder them.
 __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
@@ -411,8 +423,17 @@ static __device__ unsigned long long zc_tl[kTlSlots][kTlCtas];
       zc_tl[slot][blockIdx.x] = t_;                                          \
     }                                                                        \
   } while (0)
+#define ZC_TL_SMID(slot)                                                     \
+  do {                                                                       \
+    if (threadIdx.x == 0 && blockIdx.x < kTlCtas) {                          \
+      unsigned s_;                                                           \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(s_));                         \
+      zc_tl[slot][blockIdx.x] = s_;                                          \
+    }                                                                        \
+  } while (0)
 #else
 #define ZC_TL(slot, thread) do {} while (0)
+#define ZC_TL_SMID(slot) do {} while (0)
 #define ZC_TL_EXPORT(name)
 #endif
 void prof_mark(int tag, bool end, cudaStream_t st);

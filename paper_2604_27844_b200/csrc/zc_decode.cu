@@ -387,6 +387,7 @@ decode_ring_kernel(const DecodeSegs segs, const DChunkPlan cp, uint16_t* __restr
 
   const int tid = threadIdx.x;
   ZC_TL(0, 0);
+  ZC_TL_SMID(2);
   if (tid >= 32 && tid < 32 + 256) {
     const int v = tid - 32;   // byte -> nibble spread: bit k -> bit 4k
     uint32_t sp = 0;

@@ -347,6 +347,7 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     if (same) return;
   }
   ZC_TL(2, 0);
+  ZC_TL_SMID(3);
   extern __shared__ __align__(128) uint8_t s_dyn[];
   uint8_t* ring = s_dyn;                                              // kStages x 8 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + kStages * kStageBytes);
@@ -367,13 +368,17 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
   uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
   const int gsl = segs.gs_log2;
 
-  if (tid < 7) s_book[tid] = book[tid];
+  // (launched behind the guess kernel with PDL: the ring fills while the
+  // guess finishes; the fix-up kernel behind may be scheduled from here on)
+  grid_dep_launch();
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(bars + i, 1);
     fence_mbar_init();
     for (int i = 0; i < kStages; ++i)
       if (t_begin + i < t_end) encode_issue(xs, n, t_begin + i, ring + i * kStageBytes, bars + i);
   }
+  grid_dep_wait();
+  if (tid < 7) s_book[tid] = book[tid];
   __syncthreads();
   {
     // spread LUT (codec.py:131-138 encode_table): bit0/8/16 = code bits, bit24 = escape
@@ -702,7 +707,13 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     }
   }
   ZC_TL(5, 0);
-  if (tid == 0) run_total[blockIdx.x] = run;
+  // run total + 1 (0 = not yet published): the fix-up of a later run may be
+  // running already (PDL) and polls it; everything the CTA wrote precedes it
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release_u64(run_total + blockIdx.x, (uint64_t)run + 1u);
+  }
   if (kSums) {
     sums_block_finish(s1, s2, spec.parts + blockIdx.x);
     __shared__ bool s_last;
@@ -730,8 +741,9 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
 __global__ void __launch_bounds__(kThreads)
 encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __restrict__ book,
                      uint8_t* __restrict__ frames, const uint8_t* __restrict__ scratch,
-                     const uint64_t* __restrict__ run_total,
-                     const uint8_t* __restrict__ skip_if_same, uint64_t* __restrict__ frame_len) {
+                     const uint64_t* run_total,
+                     const uint8_t* __restrict__ skip_if_same, uint64_t* __restrict__ frame_len,
+                     int spin) {
   if (skip_if_same != nullptr) {   // same condition as the pass-1 launch it follows
     bool same = true;
 #pragma unroll
@@ -744,6 +756,19 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
   int seg;
   int64_t t_begin, t_end;
   run_range(segs, rp, blockIdx.x, seg, t_begin, t_end);
+  ZC_TL(0, 0);
+  if (spin) {
+    // launched with PDL behind pass 1 (zeroed totals): this run's own pass-1
+    // CTA must have published before its group_index / escapes are read
+    if (tid == 0) {
+      unsigned ns = 64;
+      while (ld_acquire_u64(run_total + blockIdx.x) == 0) {
+        __nanosleep(ns);
+        if (ns < 2048) ns *= 2;
+      }
+    }
+    __syncthreads();
+  }
   if (tid < 7) s_book[tid] = book[tid];
   const int gsl = segs.gs_log2;
   const int64_t n = segs.n[seg];
@@ -751,7 +776,7 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
   uint8_t* frame = frames + segs.frame_off[seg];
   uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
   const uint8_t* esc_out = scratch + (segs.tile_start[seg] + t_begin) * kTile;   // 16-B aligned
-  const uint32_t run = (uint32_t)run_total[blockIdx.x];
+  const uint32_t run = (uint32_t)(ld_relaxed_u64(run_total + blockIdx.x) - 1u);
   const int64_t e0 = t_begin * kTile;
   const int64_t e1 = (t_end * kTile < n) ? t_end * kTile : n;
   const int64_t g0 = (e0 + (int64_t(1) << gsl) - 1) >> gsl;
@@ -763,21 +788,28 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
 #pragma unroll
   for (int k = 0; k < kGiPer; ++k) {
     const int64_t g = g0 + tid + (int64_t)k * kThreads;
-    gv[k] = (gi_fast && g < g1) ? gi[g] : 0u;
+    gv[k] = (gi_fast && g < g1) ? __ldcg(gi + g) : 0u;
   }
   const bool esc_fast = run <= 16u * kThreads;
   uint4 ev = make_uint4(0, 0, 0, 0);
   if (esc_fast && 16u * tid + 16u <= run) {
-    ev = *reinterpret_cast<const uint4*>(esc_out + 16 * tid);
+    ev = __ldcg(reinterpret_cast<const uint4*>(esc_out + 16 * tid));
   } else if (esc_fast && 16u * tid < run) {   // the run's last partial 16 B: written bytes only
     uint32_t wv[4] = {0, 0, 0, 0};
     for (uint32_t j = 0; 16u * tid + j < run; ++j)
-      wv[j >> 2] |= (uint32_t)esc_out[16 * tid + j] << (8 * (j & 3));
+      wv[j >> 2] |= (uint32_t)__ldcg(esc_out + 16 * tid + j) << (8 * (j & 3));
     ev = make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
   // offset: the earlier runs' totals of this segment
   uint64_t acc = 0;
-  for (int r = rp.run_start[seg] + tid; r < (int)blockIdx.x; r += kThreads) acc += run_total[r];
+  for (int r = rp.run_start[seg] + tid; r < (int)blockIdx.x; r += kThreads) {
+    uint64_t v = spin ? ld_acquire_u64(run_total + r) : ld_relaxed_u64(run_total + r);
+    for (unsigned ns = 64; v == 0; ns = ns < 2048 ? 2 * ns : ns) {   // (spin only)
+      __nanosleep(ns);
+      v = ld_acquire_u64(run_total + r);
+    }
+    acc += v - 1u;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) s_red[warp] = acc;
@@ -793,7 +825,7 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
       if (g < g1 && P != 0) gi[g] = gv[k] + (uint32_t)P;
     }
   } else if (P != 0) {
-    for (int64_t g = g0 + tid; g < g1; g += kThreads) gi[g] += (uint32_t)P;
+    for (int64_t g = g0 + tid; g < g1; g += kThreads) gi[g] = __ldcg(gi + g) + (uint32_t)P;
   }
   // escapes -> frame + off5 + P
   uint8_t* dst = frame + L.off[5] + P;
@@ -813,7 +845,7 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
     const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 15u);
     const uint32_t h16 = (16u - mis) & 15u;
     const uint32_t head = run < h16 ? run : h16;
-    if (tid < head) dst[tid] = esc_out[tid];
+    if (tid < head) dst[tid] = __ldcg(esc_out + tid);
     // (with head > 0 the second load of the last 16-B word would read past
     // the run: that word goes to the byte tail instead)
     uint32_t nbody = (run - head) >> 4;
@@ -838,7 +870,7 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
           const uint32_t i = i0 + u * kThreads;
           // (word nbody too when head > 0: the last body word's neighbour,
           // inside the run by the nbody rule above)
-          a[u] = (i < nbody || (head && i == nbody)) ? __ldcs(s4 + i) : make_uint4(0, 0, 0, 0);
+          a[u] = (i < nbody || (head && i == nbody)) ? __ldcg(s4 + i) : make_uint4(0, 0, 0, 0);
         }
         // word i + 1 is the next lane's word i (lane 31 loads it itself)
 #pragma unroll
@@ -848,7 +880,7 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
           b[u].y = __shfl_down_sync(0xffffffffu, a[u].y, 1);
           b[u].z = __shfl_down_sync(0xffffffffu, a[u].z, 1);
           b[u].w = __shfl_down_sync(0xffffffffu, a[u].w, 1);
-          if (head && lane == 31 && i < nbody) b[u] = s4[i + 1];   // inside the run when head > 0
+          if (head && lane == 31 && i < nbody) b[u] = __ldcg(s4 + i + 1);   // inside the run when head > 0
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -869,13 +901,17 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
       case 2: body(std::integral_constant<int, 2>{}); break;
       default: body(std::integral_constant<int, 3>{}); break;
     }
-    for (uint32_t i = head + 16u * nbody + tid; i < run; i += kThreads) dst[i] = esc_out[i];
+    for (uint32_t i = head + 16u * nbody + tid; i < run; i += kThreads) dst[i] = __ldcg(esc_out + i);
   }
   if ((int)blockIdx.x == rp.run_start[seg + 1] - 1) {
     const uint64_t zc = P + run;
     write_header_and_pads(frame, L, zc, s_book);
     if (tid == 0) frame_len[seg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
   }
+  // work after this kernel in the stream sees pass 1 complete too (its last
+  // CTA certifies the codebook after publishing its run)
+  ZC_TL(1, 0);
+  if (spin) grid_dep_wait();
 }
 
 // Single-pass look-back path up to this many tiles, the two-kernel path
@@ -931,29 +967,48 @@ static int tiles_cap() {
     int cap1 = grid_for((const void*)encode_tiles_kernel<false>, kThreads, tiles_dyn_smem());
     const int cap2 = grid_for((const void*)encode_tiles_kernel<true>, kThreads, tiles_dyn_smem());
     if (cap2 < cap1) cap1 = cap2;   // one plan serves both (the re-encode reuses it)
+#ifdef ZC_ERUN_MULT
+    cap1 *= ZC_ERUN_MULT;           // experiments: runs per resident CTA slot
+#endif
     if (cap1 > 4096) cap1 = 4096;
     return cap1;
   });
 }
 
 // pass 1 + run fix-up; optional fused certificate (spec) / conditional
-// execution (skip_if_same) for the speculative path.  Nothing to zero.
+// execution (skip_if_same) for the speculative path.  `pdl`: both kernels
+// are launched with programmatic stream serialization -- pass 1 fills its
+// ring while the kernel before it (the guess) finishes, and each fix-up CTA
+// starts as soon as pass-1 CTAs retire and polls the runs it needs
+// (run_total must be zeroed; skip_if_same must be null).
 static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, const RunPlan& rp,
                                    const uint8_t* book, uint8_t* frames, uint8_t* w8,
                                    uint64_t* frame_len, const SpecOut* spec,
-                                   const uint8_t* skip_if_same, cudaStream_t st) {
+                                   const uint8_t* skip_if_same, cudaStream_t st,
+                                   bool pdl = false) {
   uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
   uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea + kNpArea;
   const bool timed = skip_if_same == nullptr;   // not the conditional re-encode
   if (timed) prof_mark(kProfEncode, false, st);
-  if (spec)
-    encode_tiles_kernel<true><<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
-        x, segs, rp, book, frames, scratch, run_total, *spec, skip_if_same);
-  else
-    encode_tiles_kernel<false><<<rp.nruns, kThreads, tiles_dyn_smem(), st>>>(
-        x, segs, rp, book, frames, scratch, run_total, SpecOut{}, skip_if_same);
-  encode_runfix_kernel<<<rp.nruns, kThreads, 0, st>>>(segs, rp, book, frames, scratch, run_total,
-                                                      skip_if_same, frame_len);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)rp.nruns);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = tiles_dyn_smem();
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, spec ? encode_tiles_kernel<true> : encode_tiles_kernel<false>,
+                                     x, segs, rp, book, frames, scratch, run_total,
+                                     spec ? *spec : SpecOut{}, skip_if_same);
+  if (e != cudaSuccess) return e;
+  cfg.dynamicSmemBytes = 0;
+  e = cudaLaunchKernelEx(&cfg, encode_runfix_kernel, segs, rp, book, frames,
+                         (const uint8_t*)scratch, (const uint64_t*)run_total, skip_if_same,
+                         frame_len, pdl ? 1 : 0);
+  if (e != cudaSuccess) return e;
   if (timed) prof_mark(kProfEncode, true, st);
   return cudaGetLastError();
 }
@@ -1049,20 +1104,21 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   //   [128K, 192K)   run sums of the fused encoder (16 B per run)
   //   [192K, 320K)   exact-pass partials (32 B per CTA)
   //   [320K]         guess book; [320K+64] need flag
-  //   [448K-64, 448K) counters: guess, certificate, exact pass
   uint8_t* spec = w8 + 256 + 8 * 4096;
   SumPartial* guess_parts = reinterpret_cast<SumPartial*>(spec);
   SumPartial* run_sums = reinterpret_cast<SumPartial*>(spec + 128 * 1024);
   Partial* exact_parts = reinterpret_cast<Partial*>(spec + 192 * 1024);
   uint8_t* guess = spec + 320 * 1024;
   int* need = reinterpret_cast<int*>(spec + 320 * 1024 + 64);
-  unsigned* counters = reinterpret_cast<unsigned*>(spec + 448 * 1024 - 64);
-  cudaError_t e = cudaMemsetAsync(counters, 0, 64, st);
+  // counters (guess, certificate, exact pass) in the first 64 B: one memset
+  // zeroes them and the run totals the PDL fix-up polls
+  unsigned* counters = reinterpret_cast<unsigned*>(w8);
+  cudaError_t e = cudaMemsetAsync(w8, 0, 256 + 8 * (size_t)rp.nruns, st);
   if (e != cudaSuccess) return e;
   e = launch_guess(x, ss, guess_parts, counters + 0, guess, st);
   if (e != cudaSuccess) return e;
   const SpecOut so{run_sums, counters + 1, total, book, result, need};
-  e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, &so, nullptr, st);
+  e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, &so, nullptr, st, true);
   if (e != cudaSuccess) return e;
   e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms, st);
   if (e != cudaSuccess) return e;

@@ -649,6 +649,7 @@ struct GuessPartial {
 __global__ void __launch_bounds__(kThreads)
 guess_kernel(const uint16_t* __restrict__ x, const StatSegs segs, GuessPartial* __restrict__ parts,
              unsigned* __restrict__ done, uint8_t* __restrict__ guess) {
+  grid_dep_launch();   // the encoder behind (PDL) may fill its rings meanwhile
   const int tid = threadIdx.x;
   const int64_t ntiles = segs.tile_start[segs.nseg];
   constexpr int kPerTile = kTile / kGuessStride;

@@ -374,6 +374,42 @@ def test_speculative_measured_encode_is_exact(case):
     assert book == zo.book_for(host)
 
 
+def test_speculative_encode_in_a_graph_matches_eager():
+    """One captured speculative encode replayed over contents whose
+    conditional launches return at once (guess right) and that run them
+    (guess fooled, certificate failing): each replay matches eager."""
+    n = 4096 * 1500 + 77
+    g = torch.Generator(device="cuda").manual_seed(9)
+    base = torch.randn(n, device="cuda", generator=g)
+    contents = {"gauss": base * 0.02}
+    fool = base * 1000.0
+    fool[(torch.arange(n, device="cuda") % 4096) < 16] *= 1e-6   # the guess's sample
+    contents["fools_guess"] = fool
+    contents["constant"] = torch.full((n,), 1.5, device="cuda")
+    nan = base * 3.0
+    nan[::3] = float("nan")
+    contents["nan_heavy"] = nan
+    contents = {k: engine.words_view(v.to(torch.bfloat16)) for k, v in contents.items()}
+    x = contents["gauss"].clone()
+    frames = torch.zeros(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    fn = lambda: engine.encode_measured(x, [(0, n)], 9, frames, [0], speculative=True)  # noqa: E731
+    fn()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        book, res, flen = fn()
+    for name in ["gauss", "fools_guess", "gauss", "nan_heavy", "constant", "fools_guess"]:
+        x.copy_(contents[name])
+        frames.fill_(0xA5)
+        graph.replay()
+        torch.cuda.synchronize()
+        got = bytes(frames[:int(flen.item())].cpu().numpy())
+        ref_frame, ref_book, ref_res = _measured_frame(contents[name].clone())
+        assert tuple(book[:7].tolist()) == ref_book, name
+        assert got == ref_frame, name
+        assert torch.equal(res.cpu(), ref_res), name
+
+
 def test_speculative_multi_segment_matches_prepare_frames(golden_meta):
     # per-peer frames of an all-to-all, sizes above the threshold
     rng = np.random.default_rng(3)
