@@ -109,6 +109,19 @@ __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
 __device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -409,7 +422,7 @@ enum ProfTag { kProfEncode = 0, kProfDecode = 1, kProfTags = 2 };
 // into the -DZC_TIMELINE debug library (scripts/exp/timeline.py).  One copy
 // per translation unit (no -rdc), read by zc_debug_timeline_{enc,dec}.
 #ifdef ZC_TIMELINE
-constexpr int kTlSlots = 6, kTlCtas = 8192;
+constexpr int kTlSlots = 10, kTlCtas = 8192;
 static __device__ unsigned long long zc_tl[kTlSlots][kTlCtas];
 #define ZC_TL_EXPORT(name)                                                   \
   extern "C" int name(unsigned long long* host) {                            \

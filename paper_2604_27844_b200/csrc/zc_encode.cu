@@ -319,11 +319,10 @@ __device__ __forceinline__ void encode_issue(const uint16_t* xs, int64_t n, int6
   }
 }
 
-// Fused certificate of the speculative path: every run's packed-fp32 sums,
-// and the last CTA to finish certifies the codebook (zc_stats.cuh).
+// Fused certificate of the speculative path: every run's packed-fp32 sums;
+// the fix-up of the last run certifies the codebook (zc_stats.cuh).
 struct SpecOut {
   SumPartial* parts;     // [nruns]
-  unsigned* done;        // zeroed before the launch
   int64_t total;         // words over all segments
   uint8_t* book;         // certified codebook (when *need == 0)
   double* result;        // sigma, count, path
@@ -707,26 +706,12 @@ encode_tiles_kernel(const uint16_t* __restrict__ x, const EncodeSegs segs, const
     }
   }
   ZC_TL(5, 0);
-  // run total + 1 (0 = not yet published): the fix-up of a later run may be
-  // running already (PDL) and polls it; everything the CTA wrote precedes it
+  // this run's statistic partial (kSums; certified by the fix-up of the last
+  // run), then run total + 1 (0 = not yet published): the fix-up behind
+  // (PDL) polls it.  Everything the CTA wrote precedes the release.
+  if (kSums) sums_block_finish(s1, s2, spec.parts + blockIdx.x);
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    st_release_u64(run_total + blockIdx.x, (uint64_t)run + 1u);
-  }
-  if (kSums) {
-    sums_block_finish(s1, s2, spec.parts + blockIdx.x);
-    __shared__ bool s_last;
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(spec.done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      certify_block(spec.parts, gridDim.x, spec.total, spec.book, spec.result, spec.need);
-    }
-  }
+  if (tid == 0) st_release_u64(run_total + blockIdx.x, (uint64_t)run + 1u);
   ZC_TL(4, 0);
 }
 
@@ -743,7 +728,7 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
                      uint8_t* __restrict__ frames, const uint8_t* __restrict__ scratch,
                      const uint64_t* run_total,
                      const uint8_t* __restrict__ skip_if_same, uint64_t* __restrict__ frame_len,
-                     int spin) {
+                     int spin, const SpecOut spec, int certify) {
   if (skip_if_same != nullptr) {   // same condition as the pass-1 launch it follows
     bool same = true;
 #pragma unroll
@@ -757,12 +742,17 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
   int64_t t_begin, t_end;
   run_range(segs, rp, blockIdx.x, seg, t_begin, t_end);
   ZC_TL(0, 0);
+  // the fused statistic's certificate: the last run's fix-up, once every
+  // run has published its partial
+  const bool certifier = certify && (int)blockIdx.x == rp.nruns - 1;
   if (spin) {
     // launched with PDL behind pass 1 (zeroed totals): this run's own pass-1
-    // CTA must have published before its group_index / escapes are read
-    if (tid == 0) {
+    // CTA (the certifier: every run's) must have published before its
+    // group_index / escapes (the partials) are read
+    for (int r = certifier ? tid : (tid == 0 ? (int)blockIdx.x : rp.nruns);
+         r < (certifier ? rp.nruns : (int)blockIdx.x + 1); r += kThreads) {
       unsigned ns = 64;
-      while (ld_acquire_u64(run_total + blockIdx.x) == 0) {
+      while (ld_acquire_u64(run_total + r) == 0) {
         __nanosleep(ns);
         if (ns < 2048) ns *= 2;
       }
@@ -908,8 +898,8 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
     write_header_and_pads(frame, L, zc, s_book);
     if (tid == 0) frame_len[seg] = (uint64_t)L.off[5] + (uint64_t)pad128((int64_t)zc);
   }
-  // work after this kernel in the stream sees pass 1 complete too (its last
-  // CTA certifies the codebook after publishing its run)
+  // work after this kernel in the stream sees pass 1 complete too
+  if (certifier) certify_block(spec.parts, rp.nruns, spec.total, spec.book, spec.result, spec.need);
   ZC_TL(1, 0);
   if (spin) grid_dep_wait();
 }
@@ -988,6 +978,7 @@ static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, co
                                    bool pdl = false) {
   uint64_t* run_total = reinterpret_cast<uint64_t*>(w8 + 256);
   uint8_t* scratch = w8 + 256 + 8 * 4096 + kSpecArea + kNpArea;
+  if (spec && !pdl) return cudaErrorInvalidValue;   // the certificate polls the run totals
   const bool timed = skip_if_same == nullptr;   // not the conditional re-encode
   if (timed) prof_mark(kProfEncode, false, st);
   cudaLaunchAttribute attr[1];
@@ -1007,7 +998,7 @@ static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, co
   cfg.dynamicSmemBytes = 0;
   e = cudaLaunchKernelEx(&cfg, encode_runfix_kernel, segs, rp, book, frames,
                          (const uint8_t*)scratch, (const uint64_t*)run_total, skip_if_same,
-                         frame_len, pdl ? 1 : 0);
+                         frame_len, pdl ? 1 : 0, spec ? *spec : SpecOut{}, spec ? 1 : 0);
   if (e != cudaSuccess) return e;
   if (timed) prof_mark(kProfEncode, true, st);
   return cudaGetLastError();
@@ -1060,11 +1051,12 @@ cudaError_t launch_exact_if_needed(const uint16_t*, const StatSegs&, int64_t, Pa
                                    uint8_t*, double*, const int*, int, cudaStream_t);
 
 // Measured codebook + encode.  Large inputs take the speculative path:
-//   1. guess_kernel: a codebook guessed from a uniform 1/128 sample;
+//   1. guess_kernel: a codebook guessed from a uniform 1/256 sample;
 //   2. the encoder runs with the guess and accumulates the certified packed-
 //      fp32 statistic of ALL of x on the side (same per-thread summation
-//      shape as sums_kernel, so the same error bound holds); its last CTA
-//      certifies the exact codebook (reference codebook_for semantics);
+//      shape as sums_kernel, so the same error bound holds); the fix-up of
+//      the last run certifies the exact codebook (reference codebook_for
+//      semantics);
 //   3. only if the certificate failed, the exact f64 pass runs (a launch
 //      that returns at once otherwise);
 //   4. only if the exact codebook differs from the guess, the frames are
@@ -1110,14 +1102,14 @@ cudaError_t launch_encode_auto(const uint16_t* x, const EncodeSegs& segs, const 
   Partial* exact_parts = reinterpret_cast<Partial*>(spec + 192 * 1024);
   uint8_t* guess = spec + 320 * 1024;
   int* need = reinterpret_cast<int*>(spec + 320 * 1024 + 64);
-  // counters (guess, certificate, exact pass) in the first 64 B: one memset
+  // counters (guess, exact pass) in the first 64 B: one memset
   // zeroes them and the run totals the PDL fix-up polls
   unsigned* counters = reinterpret_cast<unsigned*>(w8);
   cudaError_t e = cudaMemsetAsync(w8, 0, 256 + 8 * (size_t)rp.nruns, st);
   if (e != cudaSuccess) return e;
   e = launch_guess(x, ss, guess_parts, counters + 0, guess, st);
   if (e != cudaSuccess) return e;
-  const SpecOut so{run_sums, counters + 1, total, book, result, need};
+  const SpecOut so{run_sums, total, book, result, need};
   e = launch_two_pass(x, segs, rp, guess, frames, w8, frame_len, &so, nullptr, st, true);
   if (e != cudaSuccess) return e;
   e = launch_exact_if_needed(x, ss, total, exact_parts, counters + 2, book, result, need, sms, st);

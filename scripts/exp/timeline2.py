@@ -57,18 +57,25 @@ res = {}
 for rep in range(3):
     engine.encode_measured(w, [(0, n)], 9, frames, [0], speculative=True)
     torch.cuda.synchronize()
-    enc = np.zeros((6, 8192), dtype=np.uint64)
+    enc = np.zeros((10, 8192), dtype=np.uint64)
     assert lib.zc_debug_timeline_enc(enc.ctypes.data) == 0
     engine.decode([frames.data_ptr()], [0], None, [n], out, [0])
     torch.cuda.synchronize()
-    dec = np.zeros((6, 8192), dtype=np.uint64)
+    dec = np.zeros((10, 8192), dtype=np.uint64)
     assert lib.zc_debug_timeline_dec(dec.ctypes.data) == 0
     if rep == 2:
         res["encode_pass1"] = spread(enc[2], enc[5], enc[3])
         t0 = enc[2][enc[2] > 0].astype(np.int64).min()
-        for nm, sl in (("runfix_start", 0), ("runfix_end", 1), ("pass1_end", 5),
+        for nm, sl in (("runfix_start", 0), ("runfix_waited", 6), ("runfix_before_P", 7),
+                       ("runfix_stored", 8), ("runfix_end", 1), ("pass1_end", 5),
                        ("pass1_certified", 4)):
             v = (enc[sl][enc[sl] > 0].astype(np.int64) - t0) / 1e3
             res[nm] = [round(float(np.percentile(v, q)), 1) for q in (0, 10, 50, 90, 100)]
+        e1 = enc[1].astype(np.int64)
+        late = np.argsort(-e1)[:6]
+        res["latest_runfix_ctas"] = {
+            int(c): [round(float((enc[sl][c].astype(np.int64) - t0) / 1e3), 2)
+                     for sl in (5, 4, 0, 6, 7, 8, 1)] for c in late}
+        res["latest_runfix_cols"] = "pass1_end pass1_exit rf_start rf_waited rf_before_P rf_stored rf_end"
         res["decode"] = spread(dec[0], dec[1], dec[2])
 print(json.dumps(res, indent=1))
