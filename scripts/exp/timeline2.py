@@ -70,7 +70,8 @@ for rep in range(3):
                        ("runfix_stored", 8), ("runfix_end", 1), ("pass1_end", 5),
                        ("pass1_certified", 4)):
             v = (enc[sl][enc[sl] > 0].astype(np.int64) - t0) / 1e3
-            res[nm] = [round(float(np.percentile(v, q)), 1) for q in (0, 10, 50, 90, 100)]
+            if v.size:
+                res[nm] = [round(float(np.percentile(v, q)), 1) for q in (0, 10, 50, 90, 100)]
         e1 = enc[1].astype(np.int64)
         late = np.argsort(-e1)[:6]
         res["latest_runfix_ctas"] = {
