@@ -42,14 +42,17 @@ constexpr int64_t kSmallMaxWords = kSmallCtas * kSmallCtaWords;
 constexpr int kSmallThreads = kThreads;             // 8 warps (StatAcc block merge)
 
 struct SmallShared {                                 // static part of the encoder's smem
-  double s1, n, q;                                   // this CTA's sums (statistic)
-  int efin;                                          // exponent of a finite element
   double red[2][kSmallThreads / 32];
   int ered[kSmallThreads / 32];
-  uint32_t total;                                    // escapes of this CTA
   uint32_t gcnt[kSmallCtaWords / 512];               // per-group escape counts -> prefix
   uint8_t code[256];                                 // exponent -> code (0 = escape)
   uint8_t book[8];
+  // every CTA's partials, pushed into every CTA by remote stores before a
+  // cluster barrier: after it, all reads are local (no DSMEM read latency,
+  // and no barrier needed to keep a CTA's memory alive for its readers)
+  double x_sum[kSmallCtas], x_mean[kSmallCtas], x_n[kSmallCtas], x_q[kSmallCtas];
+  int x_e[kSmallCtas];
+  uint32_t x_total[kSmallCtas];
 };
 
 __device__ __forceinline__ void write_header(uint8_t* frame, int64_t n, int64_t zc, int gsl,
@@ -114,6 +117,7 @@ encode_small_kernel(const uint16_t* __restrict__ x, int64_t n, int64_t wpc,
   const int64_t r1 = r0 + wpc < n ? r0 + wpc : n;
   const int64_t cnt = r1 > r0 ? r1 - r0 : 0;
   const Layout L = layout_of(n, 9);
+  ZC_TL(0, 0);
 
   // ---- 1. slice -> shared memory (TMA bulk copies when 16-B aligned) ------
   __shared__ __align__(8) uint64_t s_bar;
@@ -137,12 +141,14 @@ encode_small_kernel(const uint16_t* __restrict__ x, int64_t n, int64_t wpc,
   for (int64_t i = nbulk / 2 + tid; i < cnt; i += kSmallThreads) words[i] = xs[i];
   __syncthreads();
   mbar_wait(&s_bar, 0);
+  ZC_TL(1, 0);
 
-  // ---- 2. codebook: numpy's two-pass f64 statistic, merged over the cluster
-  // mean = sum(x) / N, then M2 = sum((x - mean)^2) over the finite elements
-  // (bf16.measure_sigma, bf16.py:88-103; np.std is two-pass too), partial
-  // sums added in a fixed order (lane tree, warps, cluster ranks): no
-  // divisions on the serial path, identical on every CTA.
+  // ---- 2. codebook: the two-pass f64 statistic of each CTA's slice (sum and
+  // mean, then squared deviations from that mean, over the finite elements;
+  // bf16.measure_sigma, bf16.py:88-103), pushed to every CTA and merged in
+  // rank order: mean = sum / N, M2 = sum_r (M2_r + n_r (mean_r - mean)^2) --
+  // one cluster barrier, one division on the serial path, the same (N, M2)
+  // in every CTA.
   if (book_in == nullptr) {
     double a = 0.0, c = 0.0;
     int e_fin = -1;
@@ -155,37 +161,42 @@ encode_small_kernel(const uint16_t* __restrict__ x, int64_t n, int64_t wpc,
       }
     }
     block_sum2(a, c, e_fin, S.red);
-    if (tid == 0) { S.s1 = a; S.n = c; S.efin = e_fin; }
-  }
-  cluster.sync();                                          // sums visible
-  double mean = 0.0, N = 0.0;
-  int ce = -1;
-  if (book_in == nullptr) {
-    double S1 = 0.0;
-    for (int r = 0; r < C; ++r) {                           // rank order
-      const SmallShared* q = cluster.map_shared_rank(&S, r);
-      S1 += q->s1;
-      N += q->n;
-      if (ce < 0) ce = q->efin;
-    }
-    mean = N > 0.0 ? S1 / N : 0.0;
+    const double m = c > 0.0 ? a / c : 0.0;
     double q2 = 0.0, dummy = 0.0;
     int ed = -1;
     for (int64_t i = tid; i < cnt; i += kSmallThreads) {
       const uint32_t w = words[i];
       if ((w & 0x7F80u) != 0x7F80u) {
-        const double d = (double)__uint_as_float(w << 16) - mean;
+        const double d = (double)__uint_as_float(w << 16) - m;
         q2 = fma(d, d, q2);
       }
     }
     block_sum2(q2, dummy, ed, S.red);
-    if (tid == 0) S.q = q2;
+    if (tid < C) {                                          // lane t -> CTA t
+      SmallShared* q = cluster.map_shared_rank(&S, tid);
+      q->x_sum[rank] = a;
+      q->x_mean[rank] = m;
+      q->x_n[rank] = c;
+      q->x_q[rank] = q2;
+      q->x_e[rank] = e_fin;
+    }
   }
-  cluster.sync();                                          // deviations visible
+  cluster.sync();                    // partials visible; DSMEM is not touched again
+  ZC_TL(2, 0);
   if (tid == 0) {
     if (book_in == nullptr) {
-      double Q = 0.0;
-      for (int r = 0; r < C; ++r) Q += cluster.map_shared_rank(&S, r)->q;
+      double N = 0.0, S1 = 0.0, Q = 0.0;
+      int ce = -1;
+      for (int r = 0; r < C; ++r) {                         // rank order
+        N += S.x_n[r];
+        S1 += S.x_sum[r];
+        if (ce < 0) ce = S.x_e[r];
+      }
+      const double mean = N > 0.0 ? S1 / N : 0.0;
+      for (int r = 0; r < C; ++r) {
+        const double d = S.x_mean[r] - mean;
+        Q += S.x_n[r] > 0.0 ? fma(S.x_n[r] * d, d, S.x_q[r]) : 0.0;
+      }
       double res[3];
       finish_codebook(N, Q, ce, n, S.book, res);
       if (rank == 0) {
@@ -208,6 +219,7 @@ encode_small_kernel(const uint16_t* __restrict__ x, int64_t n, int64_t wpc,
   }
   __syncthreads();
 
+  ZC_TL(3, 0);
   // ---- 3. encode: a warp per 512-word group, 16 words per lane -------------
   const int64_t groups = (cnt + 511) / 512;
   for (int64_t g = warp; g < groups; g += kSmallThreads / 32) {
@@ -278,16 +290,18 @@ encode_small_kernel(const uint16_t* __restrict__ x, int64_t n, int64_t wpc,
       if (g0 + lane < groups) S.gcnt[g0 + lane] = carry + inc - v;
       carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    if (lane == 0) S.total = carry;
+    if (lane < C) cluster.map_shared_rank(&S, lane)->x_total[rank] = carry;
   }
-  cluster.sync();                                           // totals visible
+  ZC_TL(4, 0);
+  cluster.sync();                    // totals visible; the last DSMEM access of the kernel
+  ZC_TL(5, 0);
   uint32_t base = 0, zc = 0;
   for (int r = 0; r < C; ++r) {
-    const uint32_t t = *cluster.map_shared_rank(&S.total, r);
+    const uint32_t t = S.x_total[r];
     if (r < rank) base += t;
     zc += t;
   }
-  cluster.sync();                                           // no DSMEM reads after this
+  ZC_TL(6, 0);
 
   // ---- 4. group_index + escapes at their final places ----------------------
   uint32_t* gi = reinterpret_cast<uint32_t*>(frame + L.off[4]);
@@ -323,6 +337,7 @@ encode_small_kernel(const uint16_t* __restrict__ x, int64_t n, int64_t wpc,
     zero_range(frame, L.off[4] + 4 * L.groups, L.off[5]);
     zero_range(frame, L.off[5] + zc, L.off[5] + pad128(zc));
   }
+  ZC_TL(7, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -330,6 +345,7 @@ encode_small_kernel(const uint16_t* __restrict__ x, int64_t n, int64_t wpc,
 struct SmallDecShared {
   HeaderInfo h;
   int32_t err;
+  int32_t x_err[kSmallCtas];   // CTA 0: every CTA's first failing check (pushed)
 };
 
 __global__ void __launch_bounds__(kSmallThreads)
@@ -435,16 +451,14 @@ decode_small_kernel(const DecodeSegs segs, uint16_t* __restrict__ out, int32_t* 
     }
     if (lane == 0 && my_err != kOk) atomicMin(&S.err, my_err);
   }
-  cluster.sync();                                           // every CTA's error posted
+  __syncthreads();
+  if (tid == 0) cluster.map_shared_rank(&S, 0)->x_err[rank] = S.err;   // push to CTA 0
+  cluster.sync();                    // every CTA's error posted; the last DSMEM access
   if (rank == 0 && tid == 0) {
-    int32_t e = S.err;
-    for (int r = 1; r < C; ++r) {
-      const int32_t v = *cluster.map_shared_rank(&S.err, r);
-      if (v < e) e = v;
-    }
+    int32_t e = S.x_err[0];
+    for (int r = 1; r < C; ++r) e = S.x_err[r] < e ? S.x_err[r] : e;
     err[seg] = e;
   }
-  cluster.sync();                                           // DSMEM reads done
 }
 
 // ---------------------------------------------------------------------------
@@ -527,3 +541,5 @@ cudaError_t preload_small() {
 }
 
 }  // namespace zc
+
+ZC_TL_EXPORT(zc_debug_timeline_small)

@@ -13,7 +13,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from paper_2604_27844_b200 import engine  # noqa: E402
 
 dev = torch.device("cuda", 0)
-sizes = [int(a) for a in sys.argv[1:]] or [4, 8, 16, 32, 64, 128, 256]
+# sizes in MiB, or KiB with a "k" suffix
+sizes = [(int(a[:-1]) << 10) if a.endswith("k") else (int(a) << 20) for a in sys.argv[1:]] \
+    or [m << 20 for m in (4, 8, 16, 32, 64, 128, 256)]
 
 
 def leg_us(fn, reps=20):
@@ -34,8 +36,8 @@ def leg_us(fn, reps=20):
     return a.elapsed_time(b) / reps * 1e3
 
 
-for mib in sizes:
-    n = (mib << 20) // 2
+for nbytes in sizes:
+    n = nbytes // 2
     gen = torch.Generator(device=dev).manual_seed(1)
     w = engine.words_view((torch.randn(n, device=dev, generator=gen) * 0.02).to(torch.bfloat16))
     frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device=dev)
@@ -48,5 +50,5 @@ for mib in sizes:
     e_us, d_us = leg_us(enc), leg_us(dec)
     F = int(flen.item())
     ideal = (2 * n + F) * 2 / 6.1e12 * 1e6   # both legs at 6.1 TB/s
-    print(json.dumps({"MiB": mib, "encode_us": round(e_us, 1), "decode_us": round(d_us, 1),
+    print(json.dumps({"KiB": nbytes >> 10, "encode_us": round(e_us, 1), "decode_us": round(d_us, 1),
                       "step_us": round(e_us + d_us, 1), "hbm_floor_us": round(ideal, 1)}))

@@ -5,6 +5,7 @@ decoded words bit for bit."""
 from __future__ import annotations
 
 import hashlib
+import math
 
 import numpy as np
 import pytest
@@ -583,6 +584,43 @@ def test_small_message_path_matches_oracle(n, shift):
     out = torch.empty(n + 3, dtype=torch.int16, device="cuda")[3:]      # misaligned output
     err = engine.decode([f2.data_ptr()], [0], None, [n], out, [0], groups512=True)
     assert int(err[0].item()) == engine.ERR_OK and torch.equal(out, x)
+
+
+@pytest.mark.parametrize("case", ["nan_slice", "constant", "scales", "offset_mean", "one_finite"])
+def test_small_statistic_merge_edge_cases(case):
+    """The one-launch encoder merges per-CTA (sum, mean, M2) partials: slices
+    without a finite element, a zero variance (modal fallback), CTAs whose
+    scales and means differ by orders of magnitude.  Book and frame equal
+    the oracle's, sigma within 1e-12 of numpy's two-pass np.std."""
+    n = 100_000                                    # 8 CTAs of 12 800 words
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal(n) * 0.02
+    if case == "nan_slice":
+        v[:40_000] = np.nan                        # the first CTAs see no finite value
+    elif case == "constant":
+        v[:] = 0.75
+    elif case == "scales":
+        v[: n // 2] *= 1e5                         # the between-CTA term dominates M2
+    elif case == "offset_mean":
+        v += 300.0
+    elif case == "one_finite":
+        v[:] = np.inf
+        v[77_777] = 3.0
+    words = zo.from_f64(v)
+    x = torch.from_numpy(words.view(np.int16)).cuda()
+    want_book = zo.book_for(words)
+    f = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    b, res, flen = engine.encode_measured(x, [(0, n)], 9, f, [0])
+    assert tuple(b[:7].cpu().tolist()) == want_book
+    assert bytes(f[:int(flen.item())].cpu().numpy()) == zo.encode(words, want_book)
+    fin = zo.to_f32(words).astype(np.float64)
+    fin = fin[np.isfinite(fin)]
+    sigma = float(res[0].item())
+    if fin.size:
+        ref = float(np.std(fin))
+        assert sigma == pytest.approx(ref, rel=1e-12, abs=0.0 if ref else 1e-300)
+    else:
+        assert math.isnan(sigma)
 
 
 def test_small_decoder_rejects_foreign_group_size_and_corruption():
