@@ -470,13 +470,14 @@ static int small_ctas_for(int64_t n) {
   return (int)c;
 }
 
-// Measured crossover (scripts/exp/small_parts.py, graph replay): the one-launch
-// encoder wins up to 256 KiB (12.4 vs 16.2 us codebook + encode), the
-// two-pass encoder with 148 SMs from 512 KiB on (16.4 vs 18.7 us).
+// Measured crossover (bench.py --workload sweep, graph replay, push-based
+// DSMEM exchange): the one-launch encoder wins up to 512 KiB (23.2 vs
+// 24.6 us per codec step), the two-pass encoder with 148 SMs at 1 MiB
+// (25.4 vs 35.4 us).
 bool small_encode_ok(int64_t n, int gsl) {
   static const int64_t lim = [] {
     const char* e = getenv("ZC_SMALL_MAX_WORDS");
-    return e ? (int64_t)atoll(e) : (int64_t)131072;
+    return e ? (int64_t)atoll(e) : (int64_t)262144;
   }();
   return gsl == 9 && n >= 1 && n <= lim && n <= kSmallMaxWords;
 }

@@ -560,7 +560,7 @@ def test_zbf16_round_trip(tmp_path):
 
 
 @pytest.mark.parametrize("n", [1, 15, 511, 512, 513, 4095, 4096, 4097, 12_345, 65_536,
-                               131_071, 131_072, 131_073])
+                               131_071, 131_072, 131_073, 262_143, 262_144, 262_145])
 @pytest.mark.parametrize("shift", [0, 1, 8])
 def test_small_message_path_matches_oracle(n, shift):
     """One-launch cluster encoder / decoder (zc_small.cu) at the sizes around
