@@ -34,6 +34,16 @@ for n, gs in [(1, 512), (1000, 16), (4096 * 20 + 7, 512), (4096 * 40, 2048), (70
     ng = (n + gs - 1) // gs
     assert torch.equal(zc.decompress_group(chunk, ng - 1), x[(ng - 1) * gs:])
     checks += 1
+# one-launch small encoder / decoder (clusters, DSMEM pushes): measured
+# codebook + encode, decode with the 512-group flag
+for n in (100, 100_000, 262_144):
+    x = words(n)
+    frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    book, res, flen = engine.encode_measured(x, [(0, n)], 9, frames, [0])
+    out = torch.empty_like(x)
+    err = engine.decode([frames.data_ptr()], [0], None, [n], out, [0], groups512=True)
+    assert int(err[0].item()) == engine.ERR_OK and torch.equal(out, x)
+    checks += 1
 # speculative path (>= 1024 tiles): certified, and a guess the sample gets wrong
 n = 4096 * 1100 + 3
 for case in ("gauss", "fool"):
