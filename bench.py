@@ -407,7 +407,7 @@ def run_ours(args):
             if rec:
                 ev["d1"][-1].record(stream)
             return err_buf
-        # guess (1/256 sample), encoder pass 1 with the fused statistic and
+        # guess (1/512 sample), encoder pass 1 with the fused statistic and
         # certificate, run fix-up, then exact-statistic / re-encode pass 1 /
         # re-encode fix-up launches that return at once when the certificate
         # decided and the guess held, decoder init (error words + chunk
@@ -584,7 +584,7 @@ def run_ours(args):
                                 "traffic": traffic_of(k)}
                             for k, v in per.items()},
                 "encode_leg_ms": enc_leg, "decode_leg_ms": dec_leg,
-                "encode_leg_note": "codebook_for+compress: guess kernel (1/256 sample), encoder "
+                "encode_leg_note": "codebook_for+compress: guess kernel (1/512 sample), encoder "
                                    "pass 1 with the statistic fused + run fix-up, three "
                                    "conditional launches"}
     else:

@@ -101,7 +101,7 @@ int zc_encode(const uint16_t* x, const int64_t* seg_off, const int64_t* seg_n,
  * over the concatenation of the segments, one frame per segment.  flags bit 0
  * (ZC_ENCODE_SPECULATIVE, what the Python layer passes) selects the
  * speculative path for inputs of >= 1024 tiles: a codebook guessed from a
- * uniform 1/128 sample, the encoder run with it while it accumulates the
+ * uniform 1/512 sample, the encoder run with it while it accumulates the
  * certified packed-fp32 statistic of all of x, the exact f64 pass only if the
  * certificate fails and a re-encode only if the exact codebook differs from
  * the guess -- identical output, one pass over x fewer (measured 176 vs

@@ -1051,7 +1051,7 @@ cudaError_t launch_exact_if_needed(const uint16_t*, const StatSegs&, int64_t, Pa
                                    uint8_t*, double*, const int*, int, cudaStream_t);
 
 // Measured codebook + encode.  Large inputs take the speculative path:
-//   1. guess_kernel: a codebook guessed from a uniform 1/256 sample;
+//   1. guess_kernel: a codebook guessed from a uniform 1/512 sample;
 //   2. the encoder runs with the guess and accumulates the certified packed-
 //      fp32 statistic of ALL of x on the side (same per-thread summation
 //      shape as sums_kernel, so the same error bound holds); the fix-up of

@@ -631,16 +631,24 @@ cudaError_t launch_codebook_modal(const uint16_t* x, const StatSegs& segs, int64
 
 // ---- speculative encoder support (launch_encode_auto) -------------------------
 // Guess for the speculative encoder: the analytic codebook of packed-fp32
-// sums over a uniform element sample -- one 32-B sector (16 words) every
-// kGuessStride words, i.e. 1/256 of the bytes (one sector per tile: half the
-// DRAM lines of 1/128 for a sigma estimate still within ~0.1 %), spread over the whole input
-// so that no region is over-weighted (a tile sample would be fooled by a
-// small cluster, e.g. the RMSNorm vectors at the end of a layer shard).  No
-// certificate: a wrong guess only costs a re-encode.
+// sums over a uniform element sample -- one 32-B sector (16 words) from every
+// ZC_GTILESKIP-th 4096-word tile, i.e. 1/512 of the bytes by default, spread
+// over the whole input so that no region is over-weighted (a tile sample
+// would be fooled by a small cluster, e.g. the RMSNorm vectors at the end of
+// a layer shard).  No certificate: a wrong guess only costs a re-encode.
+// Sample density against the guess's latency (encode leg of the bench layer,
+// scripts/exp/guess_time.py): every tile 153.8-154.2 us, every 2nd
+// 152.2-152.8, every 4th 152.1-152.8; sigma of the 1/512 sample is within
+// ~0.15 % for Gaussian data, so a guess off the certified book (a re-encode,
+// ~140 us) needs sigma within ~0.2 % of a base flip: expected cost < 0.5 us.
 #ifndef ZC_GSTRIDE
 #define ZC_GSTRIDE 4096
 #endif
+#ifndef ZC_GTILESKIP
+#define ZC_GTILESKIP 2
+#endif
 constexpr int kGuessStride = ZC_GSTRIDE;
+constexpr int kGuessTileSkip = ZC_GTILESKIP;
 static_assert(kTile % kGuessStride == 0, "probes per tile");
 struct GuessPartial {
   double s1, s2, cnt;
@@ -653,7 +661,7 @@ guess_kernel(const uint16_t* __restrict__ x, const StatSegs segs, GuessPartial* 
   const int tid = threadIdx.x;
   const int64_t ntiles = segs.tile_start[segs.nseg];
   constexpr int kPerTile = kTile / kGuessStride;
-  const int64_t nprobe = ntiles * kPerTile;
+  const int64_t nprobe = (ntiles + kGuessTileSkip - 1) / kGuessTileSkip * kPerTile;
   // shift word K (the first element; every thread reads the same one), read
   // after the first probe's load is in flight: both round trips overlap
   uint32_t kw = 0;
@@ -667,7 +675,7 @@ guess_kernel(const uint16_t* __restrict__ x, const StatSegs segs, GuessPartial* 
   };
   double s1 = 0.0, s2 = 0.0, cnt = 0.0;
   for (int64_t p = (int64_t)blockIdx.x * kThreads + tid; p < nprobe; p += (int64_t)gridDim.x * kThreads) {
-    const int64_t tile = p / kPerTile;
+    const int64_t tile = p / kPerTile * kGuessTileSkip;
     const int sg = find_seg(segs.tile_start, segs.nseg, tile);
     const int64_t off = (tile - segs.tile_start[sg]) * kTile + (p % kPerTile) * kGuessStride;
     const int64_t nvalid = segs.n[sg] - off;
@@ -741,7 +749,8 @@ __global__ void fixed_guess_kernel(uint8_t* guess) {
 #endif
 cudaError_t launch_guess(const uint16_t* x, const StatSegs& segs, void* parts, unsigned* done,
                          uint8_t* guess, cudaStream_t st) {
-  const int64_t nprobe = segs.tile_start[segs.nseg] * (kTile / kGuessStride);
+  const int64_t nprobe = (segs.tile_start[segs.nseg] + kGuessTileSkip - 1) / kGuessTileSkip *
+                        (kTile / kGuessStride);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
