@@ -51,7 +51,7 @@ for case in ("gauss", "fool"):
     if case == "fool":
         v = v * 1000.0
         t = torch.arange(n, device="cuda")
-        v[(t % 2048) < 16] *= 1e-6          # exactly the guess kernel's sampled sectors
+        v[(t % 8192) < 16] *= 1e-6          # exactly the guess kernel's sampled sectors
     x = engine.words_view(v.to(torch.bfloat16))
     frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
     book, res, flen = engine.encode_measured(x, [(0, n)], 9, frames, [0])

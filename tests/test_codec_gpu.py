@@ -346,7 +346,7 @@ def _measured_frame(x):
 
 
 @pytest.mark.parametrize("case", ["gauss", "sample_fools_guess", "constant", "nan_heavy",
-                                  "outliers"])
+                                  "outliers", "misaligned"])
 def test_speculative_measured_encode_is_exact(case):
     n = 4096 * 1500 + 77          # above the speculative threshold (1024 tiles)
     g = torch.Generator(device="cuda").manual_seed(5)
@@ -354,10 +354,10 @@ def test_speculative_measured_encode_is_exact(case):
     if case == "gauss":
         v = v * 0.02
     elif case == "sample_fools_guess":
-        # every 32nd tile (the sampled ones) tiny, the rest large: guess != exact
+        # the guess kernel's sampled sectors (the first 16 words of every
+        # second tile) tiny, the rest large: guess != exact, re-encode
         v = v * 1000.0
-        t = torch.arange(n, device="cuda") // 4096
-        v[(t % 32) == 0] *= 1e-6
+        v[(torch.arange(n, device="cuda") % 8192) < 16] *= 1e-6
     elif case == "constant":
         v = torch.full((n,), 1.5, device="cuda")
     elif case == "nan_heavy":
@@ -367,6 +367,8 @@ def test_speculative_measured_encode_is_exact(case):
         v = v * 1e-3
         v[::997] *= 1e4
     x = engine.words_view(v.to(torch.bfloat16))
+    if case == "misaligned":      # 2-B aligned only: no TMA for any tile, odd tail
+        x = x[1:]
     frame, book, res = _measured_frame(x)
     ref_book = zc.codebook_for(x)
     assert book == ref_book.entries
