@@ -101,7 +101,8 @@ bool debug_on() {
 }
 
 // flags
-constexpr int kPlaneP2P = 1, kPlaneMsg = 2, kA2AD1 = 4, kCheckCounts = 8, kPipeline = 16;
+[[maybe_unused]] constexpr int kPlaneP2P = 1;   // the default plane (header ZC_PLANE_P2P)
+constexpr int kPlaneMsg = 2, kA2AD1 = 4, kCheckCounts = 8, kPipeline = 16;
 
 int64_t pad128h(int64_t x) { return (x + 127) / 128 * 128; }
 int64_t tiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
@@ -1332,6 +1333,8 @@ int zc_comm_reserve(zc_comm* c, int64_t slot_bytes, void* stream) {
   return p2p_grow(c, slot_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// The peer-memory plane is the default when the communicator has it
+// (ZC_PLANE_P2P only names it); ZC_PLANE_MSG forces the message plane.
 static bool use_p2p(zc_comm* c, int flags) {
   if (flags & kPlaneMsg) return false;
   return c->p2p;
