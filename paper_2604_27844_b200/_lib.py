@@ -144,8 +144,12 @@ def ptrs(vals) -> ctypes.Array:
 
 
 def stream_ptr(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    """cudaStream_t of ``stream``, else of the current device's current stream
+    (read straight from torch's C++ state: a torch.cuda.Stream object per call
+    costs several microseconds of host time on every small-message launch)."""
+    if stream is not None:
+        return int(stream.cuda_stream)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 TILE = 4096

@@ -446,10 +446,11 @@ def compress(data, codebook: ExponentCodebook, group_size: int = GROUP_SIZE) -> 
     gs = _check_group_size(group_size)
     gsl = gs.bit_length() - 1
     frames = torch.empty(engine.max_frame_bytes(n, gsl), dtype=torch.uint8, device=words.device)
-    flen = engine.encode(words, [(0, n)], codebook.device_tensor(words.device), gsl, frames, [0])
-    info = torch.cat([flen.view(torch.uint8), frames[16:24]]).cpu().numpy()
-    length = int(info[:8].view("<i8")[0])
-    zc = int(info[8:16].view("<u8")[0])
+    engine.encode(words, [(0, n)], codebook.device_tensor(words.device), gsl, frames, [0])
+    # one 8-byte read-back: the header's zero_count; the frame length follows
+    # from the size law (container.py:52-62)
+    zc = int(frames[16:24].cpu().numpy().view("<u8")[0])
+    length = engine.static_bytes(n, gsl) + -(-zc // 128) * 128
     if zc >= 1 << 32:
         raise UnrepresentableError("zero_count does not fit the 32-bit group index")
     return CompressedChunk._wrap(frames[:length], n, gs, codebook, zc)

@@ -39,9 +39,11 @@ class _Workspace:
     driving the same stream could otherwise interleave their kernels over the
     shared scratch)."""
 
-    def __init__(self, buf, lock):
-        self.buf, self.lock = buf, lock
-        self._guard = None
+    __slots__ = ("buf", "lock", "index", "_prev")
+
+    def __init__(self, buf, lock, index):
+        self.buf, self.lock, self.index = buf, lock, index
+        self._prev = None
 
     def data_ptr(self):
         return self.buf.data_ptr()
@@ -53,13 +55,22 @@ class _Workspace:
         self.lock.acquire()
         # launches inside go to the tensors' device and its current stream,
         # whatever device is current in the calling thread
-        self._guard = torch.cuda.device(self.buf.device)
-        self._guard.__enter__()
+        prev = torch._C._cuda_getDevice()
+        if prev != self.index:
+            torch._C._cuda_setDevice(self.index)
+            self._prev = prev
         return self
 
     def __exit__(self, *exc):
-        self._guard.__exit__(*exc)
+        if self._prev is not None:
+            torch._C._cuda_setDevice(self._prev)
+            self._prev = None
         self.lock.release()
+
+
+@functools.lru_cache(maxsize=4096)
+def _workspace_bytes(total_elems: int, nseg: int) -> int:
+    return int(lib().zc_workspace_bytes(total_elems, nseg))
 
 
 def workspace(total_elems: int, nseg: int, device, stream=None) -> _Workspace:
@@ -67,17 +78,25 @@ def workspace(total_elems: int, nseg: int, device, stream=None) -> _Workspace:
     so steady-state calls (and CUDA-graph captures) allocate nothing; calls on
     one stream are ordered, so reuse is safe as long as each call's launches
     are enqueued under the workspace lock (``with workspace(...) as ws:``)."""
-    nbytes = int(lib().zc_workspace_bytes(int(total_elems), int(nseg)))
-    dev = torch.device(device)
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
-    key = (dev.index, int(s.cuda_stream))
-    with _WS_GUARD:
-        lock = _WS_LOCKS.setdefault(key, threading.RLock())
-        buf = _WS.get(key)
-        if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
-            _WS[key] = buf
-    return _Workspace(buf, lock)
+    nbytes = _workspace_bytes(int(total_elems), int(nseg))
+    index = device.index if isinstance(device, torch.device) else torch.device(device).index
+    if index is None:
+        index = torch._C._cuda_getDevice()
+    s = int(stream.cuda_stream) if stream is not None else torch._C._cuda_getCurrentRawStream(index)
+    key = (index, s)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        with _WS_GUARD:
+            buf = _WS.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8,
+                                  device=torch.device("cuda", index))
+                _WS[key] = buf
+    lock = _WS_LOCKS.get(key)
+    if lock is None:
+        with _WS_GUARD:
+            lock = _WS_LOCKS.setdefault(key, threading.RLock())
+    return _Workspace(buf, lock, index)
 
 
 @functools.lru_cache(maxsize=1024)
