@@ -205,6 +205,14 @@ def measure_sigma(data) -> float:
     sigma, count, _ = result.cpu().tolist()
     if count == 0:
         raise DegenerateDataError("measure_sigma: no finite elements")
+    if count < words.numel():
+        # the reference takes np.std of the compacted finite values: numpy's
+        # pairwise tree runs over their indices, so compact on the device
+        # (order kept) and take the numpy-order sigma of that array
+        w = words.view(torch.int16)
+        finite = w[(w & 0x7F80) != 0x7F80]
+        _, result = engine.measured_codebook(finite, exact=True)
+        sigma = result[0].item()
     return float(sigma)
 
 

@@ -127,6 +127,7 @@ stats_kernel(const uint16_t* __restrict__ x, const StatSegs segs,
   if (s_last) {
     __threadfence();
     finalize_block(out, gridDim.x, total_words, book, result);
+    np_refine_near_flip(x, &segs, total_words, book, result, true);
   }
 }
 
@@ -339,144 +340,6 @@ __global__ void mode_kernel(const unsigned long long* __restrict__ hist, int64_t
 // fewer, and its f64 work is negligible at this size.
 constexpr int64_t kSmallExactTiles = 16;
 
-// ---- numpy-exact sigma ---------------------------------------------------------
-// The reference's sigma is np.std over the finite values (bf16.py:103), i.e.
-// numpy's _var: mean = (0.0 + S) / m, ret = (0.0 + Q) / m, sigma = sqrt(ret),
-// with S = pairwise_sum(v), Q = pairwise_sum((v - mean)^2) and numpy's
-// pairwise_sum (numpy/_core/src/umath/loops_utils.h.src, np.add.reduce of a
-// contiguous 1-D float64 array in one inner-loop call): n < 8: 0.0 plus the
-// elements in order; n <= 128: eight accumulators r[j] = a[j], r[j] += a[i+j]
-// for i = 8, 16, .. < n - n % 8, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then
-// the remaining elements in order; n > 128: the sums of the halves split at
-// n/2 - (n/2) % 8.  These kernels evaluate exactly that tree with IEEE
-// round-to-nearest adds (no contraction), so sigma is bit-identical to the
-// reference when every element is finite (the compacted array is then x
-// itself); with non-finite elements the exact Chan pass's value stays.
-// The tree's top kNpK levels are split over 2^kNpK threads: thread t owns
-// the node reached by t's bits (MSB first) if t is that node's leftmost
-// index; it evaluates its subtree depth first (explicit stack), and the last
-// CTA combines the owners bottom-up (node = left + right).
-constexpr int kNpLeaf = 128;
-
-__device__ __forceinline__ int64_t np_left(int64_t n) {
-  const int64_t n2 = n / 2;
-  return n2 - n2 % 8;
-}
-
-// forward-only reader of the concatenated segments as float64
-struct NpCursor {
-  const uint16_t* x;
-  const StatSegs* segs;
-  int s;
-  int64_t lo, hi;                   // concatenated range of segment s
-  __device__ void init(const uint16_t* x_, const StatSegs* sg, int64_t e) {
-    x = x_;
-    segs = sg;
-    s = 0;
-    lo = 0;
-    hi = sg->n[0];
-    seek(e);
-  }
-  __device__ __forceinline__ void seek(int64_t e) {
-    while (e >= hi && s + 1 < segs->nseg) {
-      ++s;
-      lo = hi;
-      hi += segs->n[s];
-    }
-  }
-  __device__ __forceinline__ double val(int64_t e) {
-    seek(e);
-    return (double)__uint_as_float((uint32_t)x[segs->x_off[s] + (e - lo)] << 16);
-  }
-  // elements e .. e + 7
-  __device__ __forceinline__ void val8(int64_t e, double (&v)[8]) {
-    seek(e);
-    const uint16_t* p = x + segs->x_off[s] + (e - lo);
-    if (e + 8 <= hi && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-      const uint4 q = __ldcg(reinterpret_cast<const uint4*>(p));
-      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        v[2 * j] = (double)__uint_as_float(w[j] << 16);
-        v[2 * j + 1] = (double)__uint_as_float(w[j] & 0xFFFF0000u);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = val(e + j);
-    }
-  }
-};
-
-template <int kPass>
-__device__ __forceinline__ double np_term(double v, double mean) {
-  if (kPass == 0) return v;
-  const double d = __dsub_rn(v, mean);
-  return __dmul_rn(d, d);
-}
-
-template <int kPass>
-__device__ double np_leaf(NpCursor& c, int64_t start, int64_t n, double mean) {
-  if (n < 8) {
-    double r = 0.0;
-    for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, np_term<kPass>(c.val(start + i), mean));
-    return r;
-  }
-  double r[8], v[8];
-  c.val8(start, v);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = np_term<kPass>(v[j], mean);
-  int64_t i = 8;
-  const int64_t lim = n - n % 8;
-  for (; i < lim; i += 8) {
-    c.val8(start + i, v);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], np_term<kPass>(v[j], mean));
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __dadd_rn(res, np_term<kPass>(c.val(start + i), mean));
-  return res;
-}
-
-// pairwise_sum of [start, start + n): post-order walk with an explicit stack
-template <int kPass>
-__device__ double np_subtree(NpCursor& c, int64_t start, int64_t n, double mean) {
-  struct Fr {
-    int64_t start, n;
-    double lv;
-    int st;                              // 0 new, 1 left pending, 2 right pending
-  };
-  Fr stk[32];                            // depth <= log2(2^32 / 128) + 1
-  int sp = 0;
-  stk[sp++] = Fr{start, n, 0.0, 0};
-  double ret = 0.0;
-  bool have = false;                     // a finished child's value is in ret
-  while (sp > 0) {
-    Fr& f = stk[sp - 1];
-    if (have) {
-      if (f.st == 1) {                   // left done: keep it, descend right
-        f.lv = ret;
-        f.st = 2;
-        have = false;
-        const int64_t L = np_left(f.n);
-        stk[sp++] = Fr{f.start + L, f.n - L, 0.0, 0};
-      } else {                           // right done: left + right, up one level
-        ret = __dadd_rn(f.lv, ret);
-        --sp;
-      }
-      continue;
-    }
-    if (f.n <= kNpLeaf) {
-      ret = np_leaf<kPass>(c, f.start, f.n, mean);
-      --sp;
-      have = true;
-      continue;
-    }
-    f.st = 1;
-    stk[sp++] = Fr{f.start, np_left(f.n), 0.0, 0};
-  }
-  return ret;
-}
 
 // grid = kNpOwners / kThreads.  Runs only when the exact pass saw every
 // element finite and sigma > 0 (and, behind the certificate, when it failed).
@@ -513,7 +376,7 @@ np_sigma_kernel(const uint16_t* __restrict__ x, const StatSegs segs, int64_t tot
   double mine = 0.0;
   if (owner) {
     NpCursor c;
-    c.init(x, &segs, start);
+    c.init(x, &segs, start, total);
     mine = np_subtree<kPass>(c, start, n, mean);
   }
   s_val[tid] = mine;

@@ -227,10 +227,15 @@ __device__ inline int clamp_base(int b) { return b < -126 ? -126 : (b > 121 ? 12
 // statistic kernels; within kFlipWindow of it the reference formula decides.
 constexpr double kFlipFrac = 0.35891885782276935;
 constexpr double kFlipWindow = 1e-4;
-__device__ inline int derive_base(double sigma) {
+// Within kNpFlipFrac of the flip in frac(x_opt) (sigma within ~7e-9
+// relative of a threshold) the f64 statistics re-derive the codebook from
+// numpy's own sigma (np_refine_near_flip); `near` reports that case.
+constexpr double kNpFlipFrac = 1e-8;
+__device__ inline int derive_base(double sigma, bool* near = nullptr) {
   const double xo = log2(sigma) + kBaseExponentOffset;
   const double lo = floor(xo), hi = ceil(xo);
   const double fr = xo - lo;
+  if (near != nullptr) *near = fabs(fr - kFlipFrac) < kNpFlipFrac;
   if (fabs(fr - kFlipFrac) > kFlipWindow) return clamp_base(fr < kFlipFrac ? (int)lo : (int)hi);
   const int base = (lo == hi || window_coverage(sigma, lo) >= window_coverage(sigma, hi))
                        ? (int)lo : (int)hi;
@@ -248,13 +253,15 @@ __device__ inline void write_window(uint8_t* book, int base) {
 // finite exponent ce): result[0] = sigma (NaN when no finite value),
 // result[1] = finite count, result[2] = path (1 analytic, 2 modal).
 __device__ inline void finish_codebook(double cn, double cq, int ce, int64_t total_words,
-                                       uint8_t* book, double* result) {
+                                       uint8_t* book, double* result, bool* near = nullptr) {
+  if (near != nullptr) *near = false;
   const double sigma = cn > 0.0 ? sqrt(cq / cn) : nan("");
   result[0] = sigma;
   result[1] = cn;
   if (cn > 0.0 && isfinite(sigma) && sigma > 0.0) {
-    write_window(book, derive_base(sigma));
+    write_window(book, derive_base(sigma, near));
     result[2] = 1.0;
+    if (near != nullptr) *near = *near && cn == (double)total_words;   // all finite
   } else {
     // modal fallback (codec.py:181-185): with sigma 0 or no finite value the
     // histogram has at most two bins, the common finite exponent and 255
@@ -344,5 +351,230 @@ struct NpWs {
 };
 constexpr int64_t kNpArea = ((int64_t)sizeof(NpWs) + 4095) / 4096 * 4096;
 constexpr int64_t kNpWsOff = 256 + 8 * 4096 + 512 * 1024;
+
+// ---- numpy-exact sigma ---------------------------------------------------------
+// The reference's sigma is np.std over the finite values (bf16.py:103), i.e.
+// numpy's _var: mean = (0.0 + S) / m, ret = (0.0 + Q) / m, sigma = sqrt(ret),
+// with S = pairwise_sum(v), Q = pairwise_sum((v - mean)^2) and numpy's
+// pairwise_sum (numpy/_core/src/umath/loops_utils.h.src, np.add.reduce of a
+// contiguous 1-D float64 array in one inner-loop call): n < 8: 0.0 plus the
+// elements in order; n <= 128: eight accumulators r[j] = a[j], r[j] += a[i+j]
+// for i = 8, 16, .. < n - n % 8, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then
+// the remaining elements in order; n > 128: the sums of the halves split at
+// n/2 - (n/2) % 8.  These kernels evaluate exactly that tree with IEEE
+// round-to-nearest adds (no contraction), so sigma is bit-identical to the
+// reference when every element is finite (the compacted array is then x
+// itself); with non-finite elements the exact Chan pass's value stays.
+// The tree's top kNpK levels are split over 2^kNpK threads: thread t owns
+// the node reached by t's bits (MSB first) if t is that node's leftmost
+// index; it evaluates its subtree depth first (explicit stack), and the last
+// CTA combines the owners bottom-up (node = left + right).
+constexpr int kNpLeaf = 128;
+
+__device__ __forceinline__ int64_t np_left(int64_t n) {
+  const int64_t n2 = n / 2;
+  return n2 - n2 % 8;
+}
+
+// forward-only reader of the concatenated segments as float64 (segs ==
+// nullptr: one segment of `total` elements at x)
+struct NpCursor {
+  const uint16_t* x;
+  const StatSegs* segs;
+  int s;
+  int64_t hi;                       // concatenated end of segment s
+  int64_t off;                      // element e of segment s is x[off + e]
+  __device__ void init(const uint16_t* x_, const StatSegs* sg, int64_t e, int64_t total) {
+    x = x_;
+    segs = sg;
+    s = 0;
+    hi = sg ? sg->n[0] : total;
+    off = sg ? sg->x_off[0] : 0;
+    seek(e);
+  }
+  __device__ __forceinline__ void seek(int64_t e) {
+    while (segs != nullptr && e >= hi && s + 1 < segs->nseg) {
+      ++s;
+      off = segs->x_off[s] - hi;
+      hi += segs->n[s];
+    }
+  }
+  __device__ __forceinline__ double val(int64_t e) {
+    seek(e);
+    return (double)__uint_as_float((uint32_t)x[off + e] << 16);
+  }
+  // elements e .. e + 7
+  __device__ __forceinline__ void val8(int64_t e, double (&v)[8]) {
+    seek(e);
+    const uint16_t* p = x + off + e;
+    if (e + 8 <= hi && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const uint4 q = __ldcg(reinterpret_cast<const uint4*>(p));
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[2 * j] = (double)__uint_as_float(w[j] << 16);
+        v[2 * j + 1] = (double)__uint_as_float(w[j] & 0xFFFF0000u);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = val(e + j);
+    }
+  }
+};
+
+template <int kPass>
+__device__ __forceinline__ double np_term(double v, double mean) {
+  if (kPass == 0) return v;
+  const double d = __dsub_rn(v, mean);
+  return __dmul_rn(d, d);
+}
+
+template <int kPass>
+__device__ double np_leaf(NpCursor& c, int64_t start, int64_t n, double mean) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, np_term<kPass>(c.val(start + i), mean));
+    return r;
+  }
+  double r[8], v[8];
+  c.val8(start, v);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = np_term<kPass>(v[j], mean);
+  int64_t i = 8;
+  const int64_t lim = n - n % 8;
+  for (; i < lim; i += 8) {
+    c.val8(start + i, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], np_term<kPass>(v[j], mean));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, np_term<kPass>(c.val(start + i), mean));
+  return res;
+}
+
+// pairwise_sum of [start, start + n): post-order walk with an explicit stack
+template <int kPass, int kDepth = 32>
+__device__ double np_subtree(NpCursor& c, int64_t start, int64_t n, double mean) {
+  struct Fr {
+    int64_t start, n;
+    double lv;
+    int st;                              // 0 new, 1 left pending, 2 right pending
+  };
+  Fr stk[kDepth];                        // depth <= log2(2^32 / 128) + 1 from the root
+  int sp = 0;
+  stk[sp++] = Fr{start, n, 0.0, 0};
+  double ret = 0.0;
+  bool have = false;                     // a finished child's value is in ret
+  while (sp > 0) {
+    Fr& f = stk[sp - 1];
+    if (have) {
+      if (f.st == 1) {                   // left done: keep it, descend right
+        f.lv = ret;
+        f.st = 2;
+        have = false;
+        const int64_t L = np_left(f.n);
+        stk[sp++] = Fr{f.start + L, f.n - L, 0.0, 0};
+      } else {                           // right done: left + right, up one level
+        ret = __dadd_rn(f.lv, ret);
+        --sp;
+      }
+      continue;
+    }
+    if (f.n <= kNpLeaf) {
+      ret = np_leaf<kPass>(c, f.start, f.n, mean);
+      --sp;
+      have = true;
+      continue;
+    }
+    f.st = 1;
+    stk[sp++] = Fr{f.start, np_left(f.n), 0.0, 0};
+  }
+  return ret;
+}
+
+// numpy's sigma by ONE CTA of kThreads threads (thread t owns the node its
+// 8 bits reach in the tree's top levels, as np_sigma_kernel with kNpK = 8),
+// both passes, every thread returns the same value.  Only for the rare call
+// whose sigma sits next to a flip threshold (np_refine_near_flip), so one SM
+// streaming the input twice is acceptable.
+template <int kDepth = 18>
+__device__ __forceinline__ double np_block_sigma(const uint16_t* x, const StatSegs* segs,
+                                                int64_t total) {
+  constexpr int K = 8;
+  static_assert((1 << K) == kThreads, "one owner index per thread");
+  __shared__ double s_val[kThreads];
+  __shared__ int8_t s_dep[kThreads];
+  const int tid = threadIdx.x;
+  int64_t start = 0, n = total;
+  int d = 0;
+  bool owner = true;
+  for (; d < K; ++d) {
+    if (n <= kNpLeaf) {
+      owner = (tid & ((1 << (K - d)) - 1)) == 0;
+      break;
+    }
+    const int64_t L = np_left(n);
+    if ((tid >> (K - 1 - d)) & 1) {
+      start += L;
+      n -= L;
+    } else {
+      n = L;
+    }
+  }
+  double v = 0.0;                          // pass 0: mean; pass 1: variance
+  for (int pass = 0; pass < 2; ++pass) {
+    double mine = 0.0;
+    if (owner) {
+      NpCursor c;                          // owners sit 8 levels down: 18 frames
+      c.init(x, segs, start, total);       // cover 2^32 elements (stack < 1 KB)
+      mine = pass ? np_subtree<1, kDepth>(c, start, n, v)
+                  : np_subtree<0, kDepth>(c, start, n, 0.0);
+    }
+    __syncthreads();                       // previous pass's s_val[0] read by all
+    s_val[tid] = mine;
+    s_dep[tid] = owner ? (int8_t)d : (int8_t)-1;
+    __syncthreads();
+    for (int dd = K - 1; dd >= 0; --dd) {
+      const int step = 1 << (K - dd);
+      if ((tid & (step - 1)) == 0 && s_dep[tid] > dd)
+        s_val[tid] = __dadd_rn(s_val[tid], s_val[tid + step / 2]);
+      __syncthreads();
+    }
+    v = __ddiv_rn(__dadd_rn(0.0, s_val[0]), (double)total);
+  }
+  return __dsqrt_rn(v);
+}
+
+// Behind an f64 statistic whose codebook thread 0 just wrote (result =
+// sigma, finite count, path): when every element is finite and sigma sits
+// next to a flip threshold (derive_base's `near`), the whole CTA evaluates numpy's
+// sigma and thread 0 re-derives the codebook from it -- the reference's
+// codebook even in the last-ulp window where summation order decides.
+// `book` / `result` may be shared memory; every thread of the CTA calls it.
+// `segs` == nullptr: one segment of `total` elements.  Inlined (an ABI call
+// would copy the segment table to the stack, and a kernel stack above the
+// 1 KB default makes the driver grow and shrink local memory per launch).
+template <int kDepth = 18>
+__device__ __forceinline__ void np_refine_near_flip(const uint16_t* x, const StatSegs* segs,
+                                                    int64_t total, uint8_t* book, double* result,
+                                                    bool write_result) {
+  __shared__ bool s_go;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double s = result[0];
+    bool near = false;
+    if (total > 0 && result[1] == (double)total && isfinite(s) && s > 0.0) derive_base(s, &near);
+    s_go = near;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double s = np_block_sigma<kDepth>(x, segs, total);
+  if (threadIdx.x == 0) {
+    if (write_result) result[0] = s;
+    write_window(book, derive_base(s));
+  }
+  __syncthreads();
+}
 
 }  // namespace zc

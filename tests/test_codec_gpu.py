@@ -61,7 +61,8 @@ def test_sigma_cases(golden_meta):
 def _np_sigma(words: np.ndarray) -> float:
     """The reference's measure_sigma (bf16.py:88-103): np.std of the finite
     values as float64."""
-    v = (words.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    with np.errstate(invalid="ignore"):              # signaling-NaN payloads
+        v = (words.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
     return float(np.std(v[np.isfinite(v)]))
 
 
@@ -691,3 +692,18 @@ def test_decode_when_ready_decodes_late_frames_and_times_out():
     codes = err.cpu().tolist()
     assert codes[0] == engine.ERR_OK and codes[1] == 20 and codes[2] == 20
     assert torch.equal(out[:sizes[0]], xs[0])
+
+
+@pytest.mark.parametrize("n", [3, 129, 8195, 100003, (1 << 20) + 5])
+def test_sigma_bit_identical_with_non_finite(n):
+    # the reference takes np.std of the COMPACTED finite values, so numpy's
+    # tree runs over their indices: measure_sigma compacts on the device and
+    # evaluates numpy's order over that array (NaN payloads, +-inf, ragged)
+    rng = np.random.default_rng(n)
+    for k in (1, 2, max(1, n // 50)):
+        w = zo.gaussian(n, 0.02, seed=n + k)
+        pos = rng.choice(n, size=min(k, n - 1), replace=False)
+        w[pos] = rng.choice(np.array([0x7FC0, 0xFFC1, 0x7F80, 0xFF80, 0x7F81], dtype=np.uint16),
+                            size=pos.size)
+        got = zc.measure_sigma(w)
+        assert got == _np_sigma(w), (n, k, got, _np_sigma(w))

@@ -190,3 +190,67 @@ def test_speculative_cluster_outside_sample_grid():
     assert book == zo.book_for(host)
     assert res[2] == PATH_CERTIFIED, res
     assert frame == zo.encode(host, book)
+
+
+def _tuned(target: float, n: int, rel: float, seed: int) -> np.ndarray:
+    """N(0, (0.9 target)^2) words plus +-a / +-b / +-c pairs (a ~ 2 sigma,
+    b = a/64, c = a/4096; pairs leave the sum unchanged) whose np.std is
+    target * (1 + rel) to ~1e-13 relative: data that sits next to a flip
+    threshold far inside the window where only the summation order decides."""
+    want = target * (1.0 + rel)
+    f64 = lambda w: (w.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    q = lambda v: float(f64(zo.from_f64(np.array([v])))[0])                         # noqa: E731
+    R = n // 4                                    # pair slots
+    base = f64(zo.gaussian(n - 2 * R, 0.9 * want, seed=seed))
+    a = q(2.0 * want)
+    b, c = a / 64.0, a / 4096.0                   # exact: powers of two apart
+    S0, Q0 = math.fsum(base), math.fsum(base * base)
+    D = ((want * want + (S0 / n) ** 2) * n - Q0) / 2.0   # sum of pair magnitudes^2 needed
+    counts = []
+    for m in (a, b):
+        k = int(D // (m * m)) - 1 if m == a else int(D // (m * m))
+        counts.append(max(k, 0))
+        D -= counts[-1] * m * m
+    counts.append(int(round(D / (c * c))))
+    assert sum(counts) <= R and min(counts) >= 0, counts
+
+    def build(kc):
+        v = np.zeros(n)
+        v[:base.size] = base
+        i = base.size
+        for m, k in zip((a, b, c), (counts[0], counts[1], kc)):
+            v[i:i + k], v[i + k:i + 2 * k] = m, -m
+            i += 2 * k
+        np.random.default_rng(seed + 1).shuffle(v)
+        return v
+    best = None
+    for kc in range(counts[2] - 3, counts[2] + 4):          # land on the closest
+        v = build(kc)
+        err = abs(float(np.std(v)) / want - 1.0)
+        if best is None or err < best[0]:
+            best = (err, v)
+    assert best[0] < 1e-12, best[0]
+    return zo.from_f64(best[1])
+
+
+@pytest.mark.parametrize("n,octave,rel", [(1 << 20, -6, 3e-11), (1 << 20, -6, -3e-11),
+                                          (1 << 20, 2, 4e-12), (1 << 23, -7, -2e-11),
+                                          (1 << 18, -6, 3e-11), (1 << 18, -9, -5e-12)])
+def test_near_flip_codebook_uses_numpy_sigma(n, octave, rel):
+    # the certificate refuses, the f64 fallback lands within 2^-30 of the flip,
+    # and the codebook is re-derived from numpy's summation order: sigma equal
+    # to np.std bit for bit on the codebook_for path (not only measure_sigma),
+    # through the multi-CTA statistic (2^20, 2^23) and the one-launch cluster
+    # encoder (2^18)
+    target = _flip_sigma(octave)
+    host = _tuned(target, n, rel, seed=n + octave)
+    v = (host.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    ref_sigma = float(np.std(v))
+    assert abs(ref_sigma / target - 1.0) < 1e-10
+    book, res, _, eres = _measure(host)
+    assert book == zo.book_for(host)
+    assert res[2] == PATH_EXACT, res
+    assert res[0] == ref_sigma == eres[0], (res, eres, ref_sigma)
+    sbook, sres, frame = _speculative(host)
+    assert sbook == zo.book_for(host) and sres[0] == ref_sigma, (sres, ref_sigma)
+    assert frame == zo.encode(host, sbook)
