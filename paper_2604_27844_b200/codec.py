@@ -193,7 +193,23 @@ def codebook_for(data, sigma: float | None = None) -> ExponentCodebook:
     words = device_words(data)
     if words.numel() == 0:
         return ExponentCodebook.from_base(-6)
-    return _book_from_device(device_codebook(words, sigma))
+    if sigma is not None:
+        return _book_from_device(device_codebook(words, sigma))
+    # one read of book + (sigma, finite count, path).  The device codebook is
+    # the reference's: certified (path 3), or from an f64 sigma re-derived in
+    # numpy's order next to a flip.  Within 1e-12 of a flip the sigma is
+    # taken in numpy's order over the compacted finite values and the
+    # codebook derived here with the reference's host formula (math.erf), so
+    # even the last-ulp erf comparison and non-finite inputs match.
+    host = engine.measured_codebook_packed(words).cpu()
+    s, _, path = host[8:].view(torch.float64).tolist()
+    if path == 1.0 and math.isfinite(s) and s > 0.0 and _near_flip(s):
+        return derive_codebook(measure_sigma(words))
+    return ExponentCodebook(tuple(int(v) for v in host[:7].tolist()))
+
+
+def _near_flip(sigma: float, rel: float = 1e-12) -> bool:
+    return derive_codebook(sigma * (1.0 - rel)).entries != derive_codebook(sigma * (1.0 + rel)).entries
 
 
 def measure_sigma(data) -> float:

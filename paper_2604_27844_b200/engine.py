@@ -137,20 +137,28 @@ def measured_codebook(words: torch.Tensor, segs=None, stream=None, exact: bool =
     Path 3 = codebook certified by the packed-fp32 pass (sigma then within
     ~2e-6 relative); `exact=True` always runs the f64 statistic.
     """
+    packed = measured_codebook_packed(words, segs, stream, exact)
+    return packed[:8], packed[8:].view(torch.float64)
+
+
+def measured_codebook_packed(words: torch.Tensor, segs=None, stream=None,
+                             exact: bool = False) -> torch.Tensor:
+    """measured_codebook into ONE uint8[32] device buffer: book in bytes
+    0..7, result (float64[3]) in bytes 8..31 -- one device-to-host copy
+    reads both."""
     if segs is None:
         segs = [(0, words.numel())]
     segs = _merge_segments(segs)
     dev = words.device
-    book = torch.empty(8, dtype=torch.uint8, device=dev)
-    result = torch.empty(3, dtype=torch.float64, device=dev)
+    packed = torch.empty(32, dtype=torch.uint8, device=dev)
     total = sum(n for _, n in segs)
     with workspace(total, len(segs), dev, stream) as ws:
         check(lib().zc_codebook_measured(
             words.data_ptr() if words.numel() else None, i64s(o for o, _ in segs),
-            i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), book.data_ptr(),
-            result.data_ptr(), SIGMA_EXACT if exact else 0, stream_ptr(stream)),
+            i64s(n for _, n in segs), len(segs), ws.data_ptr(), ws.numel(), packed.data_ptr(),
+            packed.data_ptr() + 8, SIGMA_EXACT if exact else 0, stream_ptr(stream)),
             "zc_codebook_measured")
-    return book, result
+    return packed
 
 
 def modal_codebook(words: torch.Tensor, segs=None, stream=None) -> torch.Tensor:

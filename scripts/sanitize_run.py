@@ -44,6 +44,21 @@ for n in (100, 100_000, 262_144):
     err = engine.decode([frames.data_ptr()], [0], None, [n], out, [0], groups512=True)
     assert int(err[0].item()) == engine.ERR_OK and torch.equal(out, x)
     checks += 1
+# sigma next to a flip threshold: the f64 fallback's last CTA and every CTA
+# of the cluster encoder re-derive the codebook from numpy's own sigma
+from tests.test_stats_gpu import _flip_sigma, _tuned  # noqa: E402
+for n in (1 << 18, 1 << 20):
+    host = _tuned(_flip_sigma(-6), n, 3e-11, seed=n)
+    x = torch.from_numpy(host.view(np.int16)).cuda()
+    book, res = engine.measured_codebook(x)
+    frames = torch.empty(engine.max_frame_bytes(n), dtype=torch.uint8, device="cuda")
+    engine.encode_measured(x, [(0, n)], 9, frames, [0])
+    checks += 1
+# measure_sigma with non-finite elements (device compaction + numpy order)
+x = words(100_003)
+x[77] = 0x7FC0
+zc.measure_sigma(x)
+checks += 1
 # speculative path (>= 1024 tiles): certified, and a guess the sample gets wrong
 n = 4096 * 1100 + 3
 for case in ("gauss", "fool"):

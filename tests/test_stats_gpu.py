@@ -254,3 +254,24 @@ def test_near_flip_codebook_uses_numpy_sigma(n, octave, rel):
     sbook, sres, frame = _speculative(host)
     assert sbook == zo.book_for(host) and sres[0] == ref_sigma, (sres, ref_sigma)
     assert frame == zo.encode(host, sbook)
+
+
+@pytest.mark.parametrize("n,rel,nan", [(1 << 20, 3e-13, True), (1 << 20, -3e-13, True),
+                                       (1 << 18, 2e-13, True), (1 << 20, -2e-13, False)])
+def test_public_codebook_for_next_to_flip(n, rel, nan):
+    # public codebook_for within 1e-12 of a flip: numpy-order sigma over the
+    # compacted finite values and the reference's host derivation (math.erf),
+    # with a NaN in the data (the device f64 fallback cannot take numpy's
+    # order over the compacted array)
+    import paper_2604_27844_b200 as zc
+    target = _flip_sigma(-6)
+    body = _tuned(target, n - 1 if nan else n, rel, seed=n + 5)
+    host = np.insert(body, n // 3, np.uint16(0x7FC0)) if nan else body
+    assert zc.measure_sigma(host) == _np_sigma_finite(host)
+    assert zc.codebook_for(host).entries == zo.book_for(host)
+
+
+def _np_sigma_finite(words: np.ndarray) -> float:
+    with np.errstate(invalid="ignore"):
+        v = (words.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return float(np.std(v[np.isfinite(v)]))
