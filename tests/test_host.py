@@ -126,3 +126,21 @@ def test_torch_bf16_narrowing_matches_reference_rule():
     from oracle import zc_oracle as zo
     got = zc.from_float32(f).numpy().view(np.uint16)
     assert np.array_equal(got, zo.from_f32(f.numpy()))
+
+
+def test_near_flip_window_host():
+    # codebook_for's host re-derivation window (codec._near_flip): true only
+    # within ~1e-12 of a threshold where the reference's derivation flips
+    import math
+    from oracle import zc_oracle as zo
+    lo, hi = 2.0 ** -6, 2.0 ** -5
+    b_lo = zo.derive(lo)
+    for _ in range(200):
+        mid = math.sqrt(lo * hi)
+        lo, hi = (mid, hi) if zo.derive(mid) == b_lo else (lo, mid)
+    flip = hi
+    for rel in (0.0, 3e-13, -3e-13):
+        assert codec._near_flip(flip * (1.0 + rel))
+    for rel in (5e-12, -5e-12, 1e-6, 0.3):
+        assert not codec._near_flip(flip * (1.0 + rel))
+    assert codec.derive_codebook(flip * (1 - 1e-9)).entries == zo.derive(flip * (1 - 1e-9))
