@@ -742,9 +742,33 @@ encode_runfix_kernel(const EncodeSegs segs, const RunPlan rp, const uint8_t* __r
   int64_t t_begin, t_end;
   run_range(segs, rp, blockIdx.x, seg, t_begin, t_end);
   ZC_TL(0, 0);
+#ifndef ZC_CERT_CTA
+#define ZC_CERT_CTA 1
+#endif
+#if ZC_CERT_CTA
+  // the fused statistic's certificate in a CTA of its own (grid = runs + 1),
+  // once every run has published its partial: off the last run's fix-up
+  if (certify && (int)blockIdx.x == rp.nruns) {
+    if (spin) {
+      for (int r = tid; r < rp.nruns; r += kThreads) {
+        unsigned ns = 64;
+        while (ld_acquire_u64(run_total + r) == 0) {
+          __nanosleep(ns);
+          if (ns < 2048) ns *= 2;
+        }
+      }
+      __syncthreads();
+    }
+    certify_block(spec.parts, rp.nruns, spec.total, spec.book, spec.result, spec.need);
+    if (spin) grid_dep_wait();
+    return;
+  }
+  const bool certifier = false;
+#else
   // the fused statistic's certificate: the last run's fix-up, once every
   // run has published its partial
   const bool certifier = certify && (int)blockIdx.x == rp.nruns - 1;
+#endif
   if (spin) {
     // launched with PDL behind pass 1 (zeroed totals): this run's own pass-1
     // CTA (the certifier: every run's) must have published before its
@@ -996,6 +1020,7 @@ static cudaError_t launch_two_pass(const uint16_t* x, const EncodeSegs& segs, co
                                      spec ? *spec : SpecOut{}, skip_if_same);
   if (e != cudaSuccess) return e;
   cfg.dynamicSmemBytes = 0;
+  if (spec && ZC_CERT_CTA) cfg.gridDim = dim3((unsigned)rp.nruns + 1);   // + the certificate's CTA
   e = cudaLaunchKernelEx(&cfg, encode_runfix_kernel, segs, rp, book, frames,
                          (const uint8_t*)scratch, (const uint64_t*)run_total, skip_if_same,
                          frame_len, pdl ? 1 : 0, spec ? *spec : SpecOut{}, spec ? 1 : 0);
